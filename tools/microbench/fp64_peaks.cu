@@ -1,0 +1,159 @@
+// Microbenchmarks for the B200 fp64 roofline denominators.
+// Measures: DFMA throughput, DMMA (mma.sync f64) throughput for several shapes,
+// read-only HBM stream bandwidth, device attributes. Prints one JSON object.
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+template <int CHAINS>
+__global__ void dfma_kernel(double *out, int iters, double a, double b) {
+  double acc[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc[c] = fma(acc[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+// m8n8k4 f64: A 1 reg, B 1 reg, C 2 regs per thread
+__global__ void dmma_m8n8k4(double *out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i][0] = 0; c[i][1] = 0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+// m16n8k4 f64: A 2 regs, B 1 reg, C 4 regs
+__global__ void dmma_m16n8k4(double *out, int iters) {
+  double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, b = 1.0 + threadIdx.x * 1e-4;
+  double c[6][4];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) for (int j = 0; j < 4; ++j) c[i][j] = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0), "d"(a1), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 12345.678) out[0] = s;
+}
+
+// m16n8k16 f64: A 8 regs, B 4 regs, C 4 regs
+__global__ void dmma_m16n8k16(double *out, int iters) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 1.0 + threadIdx.x * 1e-4 + i;
+  double c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) c[i][j] = 0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void read_stream(const double2 *__restrict__ x, size_t n2, double *out) {
+  double s0 = 0, s1 = 0;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    double2 v0 = __ldcs(x + i), v1 = __ldcs(x + i + stride), v2 = __ldcs(x + i + 2 * stride), v3 = __ldcs(x + i + 3 * stride);
+    s0 += v0.x + v1.x + v2.x + v3.x; s1 += v0.y + v1.y + v2.y + v3.y;
+  }
+  for (; i < n2; i += stride) { double2 v = x[i]; s0 += v.x; s1 += v.y; }
+  if (s0 + s1 == 12345.678) out[0] = s0;
+}
+
+__global__ void fill(double *x, size_t n) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) x[i] = 1e-9 * (i & 1023);
+}
+
+template <typename F>
+float time_ms(F f, int reps) {
+  cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+  f(); CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(a)); f(); CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    float ms; CK(cudaEventElapsedTime(&ms, a, b)); if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main() {
+  int dev = 0; CK(cudaSetDevice(dev));
+  cudaDeviceProp pr; CK(cudaGetDeviceProperties(&pr, dev));
+  int l2 = 0, sms = 0, clk = 0; CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
+  double *out; CK(cudaMalloc(&out, 64));
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"clock_khz\": %d, \"smem_optin\": %zu", pr.name, sms, l2, clk, pr.sharedMemPerBlockOptin);
+  // DFMA
+  {
+    const int iters = 20000, thr = 256, blocks = sms * 8;
+    float ms = time_ms([&] { dfma_kernel<8><<<blocks, thr>>>(out, iters, 0.999999, 1e-7); }, 5);
+    double fl = 2.0 * 8 * iters * (double)thr * blocks;
+    printf(", \"dfma_tflops\": %.2f", fl / ms / 1e9);
+  }
+  {
+    const int iters = 4000, thr = 256, blocks = sms * 8;
+    float ms = time_ms([&] { dmma_m8n8k4<<<blocks, thr>>>(out, iters); }, 5);
+    double fl = 2.0 * 8 * 8 * 4 * 8.0 * iters * (thr / 32) * (double)blocks;
+    printf(", \"dmma_m8n8k4_tflops\": %.2f", fl / ms / 1e9);
+  }
+  {
+    const int iters = 4000, thr = 256, blocks = sms * 8;
+    float ms = time_ms([&] { dmma_m16n8k4<<<blocks, thr>>>(out, iters); }, 5);
+    double fl = 2.0 * 16 * 8 * 4 * 6.0 * iters * (thr / 32) * (double)blocks;
+    printf(", \"dmma_m16n8k4_tflops\": %.2f", fl / ms / 1e9);
+  }
+  {
+    const int iters = 2000, thr = 256, blocks = sms * 8;
+    float ms = time_ms([&] { dmma_m16n8k16<<<blocks, thr>>>(out, iters); }, 5);
+    double fl = 2.0 * 16 * 8 * 16 * 4.0 * iters * (thr / 32) * (double)blocks;
+    printf(", \"dmma_m16n8k16_tflops\": %.2f", fl / ms / 1e9);
+  }
+  {
+    size_t n = (size_t)1 << 29;  // 4 GiB of doubles
+    double *x; CK(cudaMalloc(&x, n * 8));
+    fill<<<sms * 8, 256>>>(x, n); CK(cudaDeviceSynchronize());
+    for (int bpsm : {2, 4, 8}) {
+      float ms = time_ms([&] { read_stream<<<sms * bpsm, 512>>>((const double2 *)x, n / 2, out); }, 5);
+      printf(", \"hbm_read_gbs_b%d\": %.1f", bpsm, n * 8.0 / ms / 1e6);
+    }
+    CK(cudaFree(x));
+  }
+  printf("}\n");
+  return 0;
+}
