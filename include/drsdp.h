@@ -1,0 +1,221 @@
+/*
+ * drsdp.h — C ABI of libdrsdp.so, the B200-native (sm_100a, fp64) hot path of
+ * ManiDSDP, the dual Riemannian ADMM for unit-diagonal SDPs of arXiv 2512.04406.
+ *
+ * Citations "P:n" are line numbers of the paper's LaTeX source.
+ *
+ * The problem (DSDP), P:19-27:
+ *     inf_y  b^T y   s.t.  S = A*(y) - C  is PSD,  diag(S) = 1,
+ * with A(X) = (<A_a, X>)_a and A*(y) = sum_a y_a A_a. The library takes A as a
+ * monomial-index map: A_a is the symmetric 0/1 indicator of the positions (i, j) whose
+ * id is a, so <A_a, X> sums X over those ordered positions (off-diagonal entries count
+ * twice) and AA* = Diag(cnt) with cnt_a = number of ordered positions of a.
+ * Assumption 2 (AA* invertible) is checked: every id must own a position.
+ *
+ * Conventions
+ *  - fp64 everywhere, row-major, 0-based indices; n = matrix side, m = #constraints,
+ *    p = factor width (columns of Y).
+ *  - Every call returns a drsdp_status (0 = OK). No exception or abort crosses the ABI.
+ *    After an error drsdp_last_error(ctx) holds a one-line message. ERR_CUDA and
+ *    ERR_OOM are sticky: the context must be destroyed.
+ *  - A context is single-threaded (one host thread at a time); distinct contexts are
+ *    independent. All device work of a context runs on its one CUDA stream.
+ *  - Ownership: pointers marked HOST are read (or written) during the call only; the
+ *    library copies what it keeps. Pointers marked DEVICE are caller-owned device
+ *    memory; "BORROWED" ones must stay valid until the documented release point.
+ *  - There is no CPU fallback: without a usable CUDA device drsdp_create fails with
+ *    DRSDP_ERR_CUDA.
+ */
+#ifndef DRSDP_H
+#define DRSDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct drsdp_ctx drsdp_ctx; /* opaque; owns every device buffer it allocates */
+
+typedef enum {
+  DRSDP_OK = 0,
+  DRSDP_ERR_INVALID_ARG = 1,   /* NULL where not allowed, n <= 0, p < 1, id out of range, bad sizes */
+  DRSDP_ERR_NOT_SYMMETRIC = 2, /* map(i,j) != map(j,i), duplicate (i,j), or C not symmetric         */
+  DRSDP_ERR_SINGULAR_AAT = 3,  /* a constraint id with no position: Assumption 2 violated     */
+  DRSDP_ERR_STATE = 4,         /* wrong call order (e.g. solve before set_problem, HVP before COSTGRAD) */
+  DRSDP_ERR_CUDA = 5,          /* CUDA / cuSOLVER failure (sticky)                                    */
+  DRSDP_ERR_OOM = 6,           /* device allocation failed (sticky)                                   */
+  DRSDP_ERR_NOT_CONVERGED = 7, /* solve hit max_outer or time_limit; solution and trace retrievable   */
+  DRSDP_ERR_NUMERIC = 8        /* non-finite cost/gradient, or a zero row in a retraction              */
+} drsdp_status;
+
+/* ---------------------------------------------------------------------------------------------
+ * Lifetime
+ * ------------------------------------------------------------------------------------------- */
+
+/* Create a context on CUDA device `device`. cuda_stream is a cudaStream_t to run on (the caller
+ * keeps ownership and must keep it alive until destroy; cudaStreamLegacy = (void*)1 selects the
+ * legacy default stream), or NULL to let the context create its own non-blocking stream. */
+int drsdp_create(drsdp_ctx **out, int device, void *cuda_stream);
+void drsdp_destroy(drsdp_ctx *ctx);                 /* NULL-safe; frees all device memory      */
+const char *drsdp_last_error(const drsdp_ctx *ctx); /* valid until the next call on ctx        */
+int drsdp_sync(drsdp_ctx *ctx);                     /* wait for all work queued on ctx's stream */
+
+/* ---------------------------------------------------------------------------------------------
+ * Problem data (DSDP)
+ * ------------------------------------------------------------------------------------------- */
+
+/* General index-map problem. HOST pointers, copied.
+ *   C       n*n row-major symmetric cost matrix, or NULL meaning C = 0 (the BQP case).
+ *   row,col,cons  nnz COO triplets over the upper triangle (row <= col): position (row,col) and
+ *           its mirror belong to constraint id cons in [0, m). Each (row,col) at most once.
+ *           Positions absent from the list are unconstrained by A (they belong to no A_a).
+ *   b       length m.
+ * Errors: INVALID_ARG (sizes, ids out of range, row > col), NOT_SYMMETRIC (duplicate position
+ * or asymmetric C), SINGULAR_AAT (an id with no position, Assumption 2). */
+int drsdp_set_problem(drsdp_ctx *ctx, int64_t n, int64_t m, const double *C, int64_t nnz,
+                      const int32_t *row, const int32_t *col, const int32_t *cons,
+                      const double *b);
+
+/* Dense second-order BQP relaxation: min x^T Q x + c^T x over x in {-1,1}^d.
+ * Basis v(x) = [1, x_1..x_d, x_1x_2, .., x_{d-1}x_d] (graded-lex); one constraint per
+ * square-free monomial of degree <= 4 (graded-lex); amap(i,j) = id of the symmetric
+ * difference of the two basis monomials; b_{1} = tr Q, b_{x_i} = c_i, b_{x_ix_j} = 2 Q_ij,
+ * degree 3-4 -> 0; C = 0. n = 1 + d + d(d-1)/2, m = sum_{k<=4} C(d,k). HOST pointers:
+ * Q d*d symmetric, c length d. Requires 1 <= d <= 360 (n < 65536). */
+int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c);
+
+/* Sizes of the current problem (n, m, and the number of upper-triangle positions owned by
+ * some constraint). Any output pointer may be NULL. */
+int drsdp_get_sizes(drsdp_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_upper);
+
+/* Bit-exact export of the index map for parity tests. HOST outputs, caller-allocated:
+ *   amap     n*n int32, amap[i*n+j] = id of position (i,j), -1 if unconstrained;
+ *   seg_ptr  m+1 int64 CSR offsets into seg_pos (constraint-major);
+ *   seg_pos  n_upper uint32, upper positions packed (i<<16)|j with i <= j, sorted by
+ *            (id, i, j).   Any output may be NULL. */
+int drsdp_export_index_map(drsdp_ctx *ctx, int32_t *amap, int64_t *seg_ptr, uint32_t *seg_pos);
+
+/* ---------------------------------------------------------------------------------------------
+ * Solver parameters (Alg. 2 inputs P:319 and the constants the paper leaves open; defaults and
+ * the reading of each are listed in DESIGN.md)
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  double sigma0, sigma_min, sigma_max; /* penalty: initial value and clipping range (Eq. 5.1)  */
+  double gamma, tau1, tau2;            /* Eq. 5.1 constants, gamma > 1, tau2 >= tau1 > 0        */
+  double tol;                          /* stop when eta_max <= tol, default 1e-8         */
+  double eig_neg_tol;                  /* escape if lambda < -eig_neg_tol (1 + |lambda_max|)     */
+  double rank_tol;                     /* rank reduction: keep singular values >= rank_tol*max   */
+  double eps_scale, eps_floor;         /* inner tolerance eps_k = max(0.1 min(1,eta) eps_scale, eps_floor) on ||XY|| */
+  double time_limit_s;                 /* 0 = none                                                */
+  int32_t p0;                          /* initial factorization size                      */
+  int32_t max_outer, max_rtr, max_tcg; /* iteration caps (max_tcg <= 0: n(p-1))                   */
+  int32_t escape_max;                  /* at most this many escape eigenvectors per iteration     */
+  int32_t mode;                        /* 0 = y-eliminated ALM subproblem (default), 1 = fixed-M  */
+  uint64_t seed;                       /* Y^0 draw when no initial factor is given                */
+} drsdp_params;
+
+int drsdp_default_params(drsdp_params *out);
+int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm);
+
+/* Optional starting factor Y^0 (HOST, n*p row-major, rows are normalised by the library).
+ * Alg. 2 writes Y^0 = 0, which is not a manifold point; without this call the library
+ * draws Gaussian rows from params.seed (reading R1). */
+int drsdp_set_initial_factor(drsdp_ctx *ctx, int32_t p, const double *Y0);
+
+/* ---------------------------------------------------------------------------------------------
+ * Solve (Algorithm 2, ManiDSDP)
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t status, outer_iters, p_final, p_max;
+  int64_t rtr_iters, tcg_iters, n_costgrad, n_hvp;
+  double eta_p, eta_d, eta_g;            /* KKT residues (eta_g reading R7)          */
+  double dual_obj;                       /* b^T y                                                */
+  double primal_obj;                     /* <C, X + Diag z> + 1^T z  (PSDP objective)      */
+  double seconds;                        /* wall time of drsdp_solve                             */
+} drsdp_info;
+
+/* Runs Algorithm 2 to eta_max <= tol. Returns OK or ERR_NOT_CONVERGED (info filled either way). */
+int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info);
+
+/* Final tuple: y (m), the factor Y of S = YY^T (n*p_final; pass NULL to skip), p_final,
+ * z (n), X = X~ + D - Diag(z) (n*n). HOST outputs, caller-allocated; any may be NULL. */
+int drsdp_get_solution(drsdp_ctx *ctx, double *y, double *Y, int32_t *p, double *z, double *X);
+
+/* Per-outer-iteration trace, 13 doubles per row in the order
+ * iter, eta_p, eta_d, eta_g, eta_max, primal_obj, dual_obj, sigma, p, inner_iters, cg_iters,
+ * escape_delta, time_s.  Copies min(max_rows, available) rows; *n_rows = rows available. */
+int drsdp_get_trace(drsdp_ctx *ctx, int32_t max_rows, double *rows, int32_t *n_rows);
+
+/* ---------------------------------------------------------------------------------------------
+ * Subproblem evaluation (north-star kernels (b)+(c); bench and parity path)
+ *
+ * Fixed-M subproblem f(Y) = ||Y Y^T - M||_F^2 on the oblique manifold (Sub-k, with
+ * M = A*(y) - C - (X~ + D)/sigma: L_sigma = (sigma/2) f + const). Outputs on the f scale:
+ *   cost   f
+ *   egrad  E = 4 (Y Y^T Y - M Y)                 (Euclidean gradient)
+ *   rgrad  R = E - rowdot(E, Y) o Y = P_Y(E)     (Riemannian gradient, Lemma 4.1 / Eq. 4.6:
+ *                                                  grad Psi = (sigma/2) R = 2 X Y)
+ *   hvp    H = P_Y(4 [Z Y + (YY^T - M) U]) - rowdot(E, Y) o U,  Z = Y U^T + U Y^T
+ *          (Eq. 4.7 with y frozen, times 2/sigma)
+ * ------------------------------------------------------------------------------------------- */
+
+/* Register M (DEVICE, BORROWED until the next set_subproblem_matrix or destroy): n x n symmetric,
+ * row pitch ldm >= n doubles, 8-byte aligned base. Symmetry is the caller's
+ * contract (not re-checked). Computes ||M||_F^2 once (one pass over M). Independent of the
+ * problem set by set_problem/set_bqp. */
+int drsdp_set_subproblem_matrix(drsdp_ctx *ctx, int64_t n, const double *M_dev, int64_t ldm);
+
+enum { DRSDP_EVAL_COSTGRAD = 1, DRSDP_EVAL_HVP = 2 };
+
+/* DEVICE pointers, caller-owned, asynchronous on the ctx stream (time with CUDA events on that
+ * stream; drsdp_sync to wait). Y_dev, U_dev, egrad/rgrad/hvp are n*p row-major (pitch p).
+ * Y rows must have unit norm (not re-checked); U must be tangent at Y for the HVP to be the
+ * Riemannian Hessian. flags: COSTGRAD computes cost/egrad/rgrad (any output pointer may be NULL);
+ * HVP computes hvp and needs U_dev; HVP without COSTGRAD in the same call reuses the Gram matrix
+ * and rowdot(E, Y) cached by the last COSTGRAD call at the same Y_dev and p (else ERR_STATE).
+ * 1 <= p <= 64. */
+int drsdp_subproblem_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y_dev,
+                          const double *U_dev, double *cost_dev, double *egrad_dev,
+                          double *rgrad_dev, double *hvp_dev);
+
+/* Same evaluation from HOST buffers (copies in and out inside the call; synchronous).
+ * cost, egrad, rgrad, hvp may be NULL. Used for the end-to-end (host<->device) measurement. */
+int drsdp_subproblem_eval_host(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y,
+                               const double *U, double *cost, double *egrad, double *rgrad,
+                               double *hvp);
+
+/* ---------------------------------------------------------------------------------------------
+ * ADMM-state operator kernels (north-star (a) and (d)); DEVICE pointers, asynchronous.
+ * They use the problem set by set_problem / set_bqp.
+ * ------------------------------------------------------------------------------------------- */
+
+/* (a) M assembly: M = A*(y) - C - T / sigma (n x ld_out, DEVICE); y (m), T (n x ldt) DEVICE. */
+int drsdp_assemble_M(drsdp_ctx *ctx, const double *y_dev, const double *T_dev, int64_t ldt,
+                     double sigma, double *M_dev, int64_t ldm);
+
+/* (d) y-update (Lemma 3.1, P:116 / Alg. 2 step 5): y = (AA*)^{-1} A(Y Y^T + C),
+ * a deterministic segmented sum over the index map. Y (n x p, pitch p), y_out (m), DEVICE. */
+int drsdp_y_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, double *y_dev);
+
+/* (d) dual update (Alg. 2 steps 6-8): T <- T - sigma (A*(y) - Y Y^T - C) in place,
+ * z = rowdot(T Y, Y). Scalars (DEVICE, 4 doubles): [||A*(y) - S - C||_F, b^T y,
+ * <C,T> + 1^T z (PSDP objective), ||T||_F^2]. */
+int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const double *y_dev,
+                      double sigma, double *T_dev, int64_t ldt, double *z_dev,
+                      double *scalars_dev);
+
+/* y-eliminated (ALM) subproblem f^(Y) = ||Y Y^T + C + T/sigma||^2 - sum_a A(YY^T + C)_a^2/cnt_a
+ * and its derivatives (gradient 4 (S - M(S)) Y, HVP with the projection term of Eq. 4.7).
+ * DEVICE pointers; T (n x ldt). Same flags / outputs as drsdp_subproblem_eval. */
+int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev, int64_t ldt,
+                   double sigma, const double *Y_dev, const double *U_dev, double *cost_dev,
+                   double *egrad_dev, double *rgrad_dev, double *hvp_dev);
+
+/* Device kernel launches issued by this context since creation (for launch accounting). */
+int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRSDP_H */

@@ -218,3 +218,33 @@ class ALMProblem:
         w = ops.A(self.amap, Z, self.m) / self.cnt
         EH = 4.0 * (Z @ Y + W @ U - ops.At(self.amap, w) @ Y)
         return project(Y, EH) - rho[:, None] * U
+
+
+def fixed_rows(M_rows: np.ndarray, rows: np.ndarray, Y: np.ndarray, U: np.ndarray | None = None) -> dict:
+    """Rows `rows` of E, R (and H) of the fixed-M subproblem, for sampled checks at sizes where the
+    full n x n products do not fit the oracle's budget. M_rows = M[rows, :]. Same definitions as
+    fixed_eval restricted to those rows:
+        E_j = 4 sum_i (S_ji - M_ji) y_i,     S_ji = <y_j, y_i>
+        H_j = P_{y_j}(4 [ (Z Y)_j + ((S - M) U)_j ]) - rowdot(E, Y)_j u_j."""
+    S_rows = Y[rows] @ Y.T
+    W = S_rows - M_rows
+    E = 4.0 * (W @ Y)
+    rho = rowdot(E, Y[rows])
+    out = {"E": E, "rho": rho, "R": E - rho[:, None] * Y[rows]}
+    if U is not None:
+        Z_rows = Y[rows] @ U.T + U[rows] @ Y.T
+        EH = 4.0 * (Z_rows @ Y + W @ U)
+        yr = Y[rows]
+        out["H"] = EH - rowdot(EH, yr)[:, None] * yr - rho[:, None] * U[rows]
+    return out
+
+
+def fixed_cost_blocked(M_block_fn, Y: np.ndarray, block: int = 1024) -> float:
+    """f = ||YY^T - M||^2 accumulated over row blocks; M_block_fn(i0, i1) returns M[i0:i1, :]."""
+    n = Y.shape[0]
+    f = 0.0
+    for i0 in range(0, n, block):
+        i1 = min(n, i0 + block)
+        W = Y[i0:i1] @ Y.T - M_block_fn(i0, i1)
+        f += float(np.sum(W * W))
+    return f

@@ -1,0 +1,888 @@
+// abi.cu — extern "C" entry points of libdrsdp.so (see include/drsdp.h), problem setup and the
+// device-side subproblem evaluations (fixed-M and y-eliminated ALM).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "kernels.cuh"
+#include "symv.cuh"
+
+using namespace drsdp;
+
+namespace drsdp {
+
+int set_error(drsdp_ctx *ctx, int code, const std::string &msg) {
+  if (ctx) {
+    ctx->err = msg;
+    if (code == DRSDP_ERR_CUDA || code == DRSDP_ERR_OOM) ctx->sticky = code;
+  }
+  return code;
+}
+
+int cuda_check(drsdp_ctx *ctx, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return DRSDP_OK;
+  cudaGetLastError();
+  const int code = (e == cudaErrorMemoryAllocation) ? DRSDP_ERR_OOM : DRSDP_ERR_CUDA;
+  return set_error(ctx, code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                        \
+  do {                                                        \
+    int _rc = cuda_check(ctx, (call), what);                  \
+    if (_rc) return _rc;                                      \
+  } while (0)
+#define KL(call, what)                                        \
+  do {                                                        \
+    ctx->launches++;                                          \
+    int _rc = cuda_check(ctx, (call), what);                  \
+    if (_rc) return _rc;                                      \
+  } while (0)
+
+int choose_splits(drsdp_ctx *ctx, int n, int bn) {
+  const int ntiles = (n + bn - 1) / bn;
+  const int slots = ctx->num_sms * 2;
+  int bestS = 1;
+  double best = 1e300;
+  for (int S = 1; S <= 64; ++S) {
+    const int per = (n + S - 1) / S;
+    const int rps = ((per + 63) / 64) * 64;
+    if (S > 1 && rps < 64) break;
+    if ((int64_t)(S - 1) * rps >= n) break;  // empty splits
+    const int ctas = ntiles * S;
+    const int waves = (ctas + slots - 1) / slots;
+    const double cost = (double)waves * (rps + 32) + 16.0 * S;
+    if (cost < best * 0.999) {
+      best = cost;
+      bestS = S;
+    }
+  }
+  return bestS;
+}
+
+int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
+  const int pt = symv_pt(p);
+  // symv split partials: ntiles * S * BN * PT = ~n * S * PT (S <= 64)
+  const int bn_min = 8;
+  const int64_t ntiles = (n + bn_min - 1) / bn_min + 1;
+  const size_t symv_need = (size_t)(n + 64) * 64 * pt;
+  CK(ctx->symv_part.ensure(symv_need), "alloc symv workspace");
+  CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
+  CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
+  CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64), "alloc gram workspace");
+  return DRSDP_OK;
+}
+
+static int ensure_red(drsdp_ctx *ctx, int64_t blocks, int k) {
+  CK(ctx->red_part.ensure((size_t)blocks * k + 64), "alloc reduction workspace");
+  return DRSDP_OK;
+}
+
+int read_scalars(drsdp_ctx *ctx, int first, int count) {
+  CK(cudaMemcpyAsync(ctx->h_scal + first, ctx->d_scal + first, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                     ctx->stream),
+     "read scalars");
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  return DRSDP_OK;
+}
+
+static int gram(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const double *U, double *G, double *K,
+                double *gg) {
+  GramArgs g;
+  g.n = n;
+  g.p = p;
+  g.Y = Y;
+  g.ldy = ldv;
+  g.U = U;
+  g.ldu = ldv;
+  g.part = ctx->gram_part.ptr;
+  g.counter = ctx->counters + C_GRAM;
+  g.G = G;
+  g.K = K;
+  g.gg = gg;
+  g.max_blocks = 296;
+  KL(gram_launch(g, ctx->stream), "gram kernel");
+  return DRSDP_OK;
+}
+
+static SymvArgs base_symv(drsdp_ctx *ctx, int n, int p, const double *A, int64_t lda) {
+  SymvArgs a;
+  a.A = A;
+  a.lda = lda;
+  a.n = n;
+  a.p = p;
+  a.part = ctx->symv_part.ptr;
+  a.tile_cnt = ctx->tile_cnt.ptr;
+  a.tile_scal = ctx->tile_scal.ptr;
+  a.glob_cnt = ctx->counters + C_SYMV;
+  return a;
+}
+
+static int run_symv(drsdp_ctx *ctx, SymvArgs &a, int epi, bool gather) {
+  const int bn = symv_bn(symv_pt(a.p), gather);
+  const int S = choose_splits(ctx, a.n, bn);
+  const int per = (a.n + S - 1) / S;
+  a.rows_per_split = ((per + 63) / 64) * 64;
+  KL(symv_launch(a, epi, gather, S, ctx->stream), "symv kernel");
+  return DRSDP_OK;
+}
+
+// Fixed-M evaluation: cost/egrad/rgrad (COSTGRAD) and hvp (HVP), device pointers.
+int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t ldm, const double *Y, int ldv,
+               const double *U, double *cost, double *egrad, double *rgrad, double *hvp, double *G, double *K,
+               double *rho, const double *cost_extra_dev, bool have_gram) {
+  int rc = ensure_workspace(ctx, n, p);
+  if (rc) return rc;
+  if (flags & DRSDP_EVAL_COSTGRAD) {
+    rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
+    if (rc) return rc;
+    SymvArgs a = base_symv(ctx, n, p, M, ldm);
+    a.V = Y;
+    a.ldv = ldv;
+    a.Y = Y;
+    a.ldy = ldv;
+    a.G = G;
+    a.out = rgrad;
+    a.ldo = ldv;
+    a.egrad = egrad;
+    a.lde = ldv;
+    a.rho_out = rho;
+    a.scal_out = ctx->d_scal + S_SCAL;
+    a.gg = ctx->d_scal + S_GG;
+    a.cost_extra = cost_extra_dev;
+    a.cost_out = cost ? cost : ctx->d_scal + S_COST;
+    rc = run_symv(ctx, a, EPI_COSTGRAD, false);
+    if (rc) return rc;
+  }
+  if (flags & DRSDP_EVAL_HVP) {
+    rc = gram(ctx, n, p, Y, ldv, U, G, K, ctx->d_scal + S_GG);
+    if (rc) return rc;
+    SymvArgs a = base_symv(ctx, n, p, M, ldm);
+    a.V = U;
+    a.ldv = ldv;
+    a.Y = Y;
+    a.ldy = ldv;
+    a.U = U;
+    a.ldu = ldv;
+    a.G = G;
+    a.K = K;
+    a.rho = rho;
+    a.out = hvp;
+    a.ldo = ldv;
+    a.scal_out = ctx->d_scal + S_SCAL;
+    rc = run_symv(ctx, a, EPI_HVP, false);
+    if (rc) return rc;
+  }
+  (void)have_gram;
+  return DRSDP_OK;
+}
+
+static SegArgs seg_args(drsdp_ctx *ctx, int p, const double *Y, const double *U, int ldv, double *out) {
+  Problem &P = ctx->prob;
+  SegArgs s;
+  s.m = P.m;
+  s.seg_ptr = P.seg_ptr.ptr;
+  s.seg_pos = P.seg_pos.ptr;
+  s.cnt = P.cnt.ptr;
+  s.is_large = P.is_large.ptr;
+  s.large_ids = P.large_ids.ptr;
+  s.n_large = P.n_large;
+  s.cA = P.has_C ? P.cA.ptr : nullptr;
+  s.Y = Y;
+  s.U = U;
+  s.ld = ldv;
+  s.p = p;
+  s.out = out;
+  s.part = ctx->red_part.ptr;
+  s.counter = ctx->counters + C_SEG;
+  s.scal_out = ctx->d_scal + S_SEGSQ;
+  return s;
+}
+
+// y-eliminated subproblem at Y: y(S), M(S) (materialised into Mout), cost/gradients.
+int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y, int ldv,
+                 double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost, double *egrad,
+                 double *rgrad) {
+  Problem &P = ctx->prob;
+  const int n = (int)P.n;
+  int rc = ensure_workspace(ctx, n, p);
+  if (rc) return rc;
+  rc = ensure_red(ctx, std::max<int64_t>(segsum_blocks(P.m, P.n_large), 1184), 4);
+  if (rc) return rc;
+  rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
+  if (rc) return rc;
+  SegArgs s = seg_args(ctx, p, Y, nullptr, ldv, yS);
+  KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
+  AssembleArgs as;
+  as.n = n;
+  as.amap = P.amap.ptr;
+  as.ldmap = P.ld;
+  as.y = yS;
+  as.C = P.has_C ? P.C.ptr : nullptr;
+  as.ldc = P.ld;
+  as.T = T;
+  as.ldt = ldt;
+  as.sigma = sigma;
+  as.M = Mout;
+  as.ldm = ldm;
+  as.part = ctx->red_part.ptr;
+  as.counter = ctx->counters + C_ASM;
+  as.scal_out = ctx->d_scal + S_M0;
+  KL(assemble_launch(as, ctx->stream), "assemble kernel");
+  // cost constants: ||M0||^2 + sum a^2/cnt - 2 yS.cA
+  if (P.has_C) {
+    KL(vdot_launch(P.m, yS, P.cA.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_YCA, ctx->stream),
+       "vdot");
+    KL(combine_launch(ctx->d_scal + S_SEGSQ, 1.0, ctx->d_scal + S_YCA, -2.0, 0.0, ctx->d_scal + S_EXTRA + 1,
+                      ctx->stream),
+       "combine");
+  } else {
+    KL(combine_launch(ctx->d_scal + S_SEGSQ, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA + 1, ctx->stream),
+       "combine");
+  }
+  KL(combine_launch(ctx->d_scal + S_M0, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA, ctx->stream), "combine");
+  SymvArgs a = base_symv(ctx, n, p, Mout, ldm);
+  a.V = Y;
+  a.ldv = ldv;
+  a.Y = Y;
+  a.ldy = ldv;
+  a.G = G;
+  a.out = rgrad;
+  a.ldo = ldv;
+  a.egrad = egrad;
+  a.lde = ldv;
+  a.rho_out = rho;
+  a.scal_out = ctx->d_scal + S_SCAL;
+  a.gg = ctx->d_scal + S_GG;
+  a.cost_extra = ctx->d_scal + S_EXTRA;
+  a.cost_out = cost ? cost : ctx->d_scal + S_COST;
+  return run_symv(ctx, a, EPI_COSTGRAD, false);
+}
+
+int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
+            const double *G, double *K, const double *rho, double *wZ, double *hvp) {
+  Problem &P = ctx->prob;
+  const int n = (int)P.n;
+  int rc = gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
+  if (rc) return rc;
+  SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
+  KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
+  SymvArgs a = base_symv(ctx, n, p, M, ldm);
+  a.V = U;
+  a.ldv = ldv;
+  a.amap = P.amap.ptr;
+  a.ldm = P.ld;
+  a.w = wZ;
+  a.X = Y;
+  a.ldx = ldv;
+  a.Y = Y;
+  a.ldy = ldv;
+  a.U = U;
+  a.ldu = ldv;
+  a.G = G;
+  a.K = K;
+  a.rho = rho;
+  a.out = hvp;
+  a.ldo = ldv;
+  a.scal_out = ctx->d_scal + S_SCAL;
+  return run_symv(ctx, a, EPI_HVP, true);
+}
+
+// ----------------------------------------------------------------------------------------------
+// Problem construction
+// ----------------------------------------------------------------------------------------------
+static int finalize_problem(drsdp_ctx *ctx, const double *C_host) {
+  Problem &P = ctx->prob;
+  const int64_t n = P.n, m = P.m;
+  // counts, CSR over upper positions (constraint-major, row-major within a constraint)
+  std::vector<int64_t> cnt_upper(m, 0);
+  std::vector<int64_t> cnt_ord(m, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i; j < n; ++j) {
+      const int32_t id = P.h_amap[i * n + j];
+      if (id < 0) continue;
+      cnt_upper[id]++;
+      cnt_ord[id] += (i == j) ? 1 : 2;
+    }
+  for (int64_t a = 0; a < m; ++a)
+    if (cnt_ord[a] == 0)
+      return set_error(ctx, DRSDP_ERR_SINGULAR_AAT,
+                       "constraint " + std::to_string(a) + " has no position (Assumption 2, P:33)");
+  P.h_cnt.assign(m, 0);
+  for (int64_t a = 0; a < m; ++a) {
+    if (cnt_ord[a] > INT32_MAX) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "constraint too large");
+    P.h_cnt[a] = (int32_t)cnt_ord[a];
+  }
+  P.h_seg_ptr.assign(m + 1, 0);
+  for (int64_t a = 0; a < m; ++a) P.h_seg_ptr[a + 1] = P.h_seg_ptr[a] + cnt_upper[a];
+  P.n_upper = P.h_seg_ptr[m];
+  P.h_seg_pos.assign(P.n_upper, 0);
+  {
+    std::vector<int64_t> fill(P.h_seg_ptr.begin(), P.h_seg_ptr.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = i; j < n; ++j) {
+        const int32_t id = P.h_amap[i * n + j];
+        if (id < 0) continue;
+        P.h_seg_pos[fill[id]++] = ((uint32_t)i << 16) | (uint32_t)j;
+      }
+  }
+  std::vector<uint8_t> is_large(m, 0);
+  std::vector<int32_t> large_ids;
+  for (int64_t a = 0; a < m; ++a)
+    if (cnt_upper[a] > 32) {
+      is_large[a] = 1;
+      large_ids.push_back((int32_t)a);
+    }
+  P.n_large = (int64_t)large_ids.size();
+  // device copies
+  P.ld = ((n + 63) / 64) * 64;
+  std::vector<int32_t> amap_pad((size_t)n * P.ld, -1);
+  for (int64_t i = 0; i < n; ++i) std::memcpy(&amap_pad[i * P.ld], &P.h_amap[i * n], sizeof(int32_t) * n);
+  CK(P.amap.ensure(amap_pad.size()), "alloc amap");
+  CK(cudaMemcpy(P.amap.ptr, amap_pad.data(), sizeof(int32_t) * amap_pad.size(), cudaMemcpyHostToDevice), "copy amap");
+  CK(P.cnt.ensure(m), "alloc cnt");
+  CK(cudaMemcpy(P.cnt.ptr, P.h_cnt.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice), "copy cnt");
+  CK(P.b.ensure(m), "alloc b");
+  CK(cudaMemcpy(P.b.ptr, P.h_b.data(), sizeof(double) * m, cudaMemcpyHostToDevice), "copy b");
+  CK(P.seg_ptr.ensure(m + 1), "alloc seg_ptr");
+  CK(cudaMemcpy(P.seg_ptr.ptr, P.h_seg_ptr.data(), sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice), "copy seg_ptr");
+  CK(P.seg_pos.ensure(std::max<int64_t>(P.n_upper, 1)), "alloc seg_pos");
+  CK(cudaMemcpy(P.seg_pos.ptr, P.h_seg_pos.data(), sizeof(uint32_t) * P.n_upper, cudaMemcpyHostToDevice),
+     "copy seg_pos");
+  CK(P.is_large.ensure(m), "alloc is_large");
+  CK(cudaMemcpy(P.is_large.ptr, is_large.data(), m, cudaMemcpyHostToDevice), "copy is_large");
+  CK(P.large_ids.ensure(std::max<int64_t>(P.n_large, 1)), "alloc large_ids");
+  if (P.n_large)
+    CK(cudaMemcpy(P.large_ids.ptr, large_ids.data(), sizeof(int32_t) * P.n_large, cudaMemcpyHostToDevice),
+       "copy large_ids");
+  P.has_C = C_host != nullptr;
+  if (P.has_C) {
+    std::vector<double> cpad((size_t)n * P.ld, 0.0);
+    std::vector<double> cA(m, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        cpad[i * P.ld + j] = C_host[i * n + j];
+        const int32_t id = P.h_amap[i * n + j];
+        if (id >= 0) cA[id] += C_host[i * n + j];
+      }
+    CK(P.C.ensure(cpad.size()), "alloc C");
+    CK(cudaMemcpy(P.C.ptr, cpad.data(), sizeof(double) * cpad.size(), cudaMemcpyHostToDevice), "copy C");
+    CK(P.cA.ensure(m), "alloc cA");
+    CK(cudaMemcpy(P.cA.ptr, cA.data(), sizeof(double) * m, cudaMemcpyHostToDevice), "copy cA");
+  }
+  ctx->has_problem = true;
+  ctx->alm_cached_valid = false;
+  free_solver(ctx);
+  ctx->trace.clear();
+  return DRSDP_OK;
+}
+
+// graded-lex rank of square-free monomials of degree <= 4 over d variables
+struct MonoRank {
+  int d;
+  std::vector<int64_t> off;              // offset of degree k
+  std::vector<std::vector<int64_t>> cum;  // cum[k][x] = sum_{v < x} C(d - v - 1, k - 1)
+  static int64_t binom(int64_t a, int64_t b) {
+    if (b < 0 || a < b) return 0;
+    int64_t r = 1;
+    for (int64_t i = 1; i <= b; ++i) r = r * (a - b + i) / i;
+    return r;
+  }
+  explicit MonoRank(int d_) : d(d_) {
+    off.assign(6, 0);
+    for (int k = 0; k < 5; ++k) off[k + 1] = off[k] + binom(d, k);
+    cum.assign(5, std::vector<int64_t>(d + 1, 0));
+    for (int k = 1; k <= 4; ++k)
+      for (int x = 0; x < d; ++x) cum[k][x + 1] = cum[k][x] + binom(d - x - 1, k - 1);
+  }
+  // a: sorted indices, k = size
+  int64_t id(const int *a, int k) const {
+    int64_t r = 0;
+    int prev = -1;
+    for (int i = 0; i < k; ++i) {
+      const int kk = k - i;
+      r += cum[kk][a[i]] - cum[kk][prev + 1];
+      prev = a[i];
+    }
+    return off[k] + r;
+  }
+};
+
+}  // namespace drsdp
+
+// ==============================================================================================
+// extern "C"
+// ==============================================================================================
+extern "C" {
+
+int drsdp_create(drsdp_ctx **out, int device, void *cuda_stream) {
+  if (!out) return DRSDP_ERR_INVALID_ARG;
+  *out = nullptr;
+  drsdp_ctx *ctx = new (std::nothrow) drsdp_ctx();
+  if (!ctx) return DRSDP_ERR_OOM;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    delete ctx;
+    return DRSDP_ERR_CUDA;
+  }
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return DRSDP_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return DRSDP_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  bool ok = cudaMalloc(&ctx->counters, sizeof(unsigned) * C_TOTAL) == cudaSuccess &&
+            cudaMemset(ctx->counters, 0, sizeof(unsigned) * C_TOTAL) == cudaSuccess &&
+            cudaMalloc(&ctx->d_scal, sizeof(double) * S_TOTAL) == cudaSuccess &&
+            cudaMemset(ctx->d_scal, 0, sizeof(double) * S_TOTAL) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_scal, sizeof(double) * S_TOTAL) == cudaSuccess &&
+            cudaMalloc(&ctx->d_flag, sizeof(int)) == cudaSuccess &&
+            ctx->sub_G.ensure(2 * 64 * 64) == cudaSuccess && ctx->sub_K.ensure(64 * 64) == cudaSuccess &&
+            ctx->red_part.ensure(1 << 16) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    drsdp_destroy(ctx);
+    return DRSDP_ERR_CUDA;
+  }
+  drsdp_default_params(&ctx->prm);
+  *out = ctx;
+  return DRSDP_OK;
+}
+
+void drsdp_destroy(drsdp_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  free_solver(ctx);
+  Problem &P = ctx->prob;
+  P.amap.release();
+  P.C.release();
+  P.cA.release();
+  P.cnt.release();
+  P.b.release();
+  P.seg_ptr.release();
+  P.seg_pos.release();
+  P.is_large.release();
+  P.large_ids.release();
+  ctx->red_part.release();
+  ctx->gram_part.release();
+  ctx->symv_part.release();
+  ctx->tile_cnt.release();
+  ctx->tile_scal.release();
+  ctx->sub_G.release();
+  ctx->sub_K.release();
+  ctx->sub_rho.release();
+  ctx->alm_M.release();
+  ctx->alm_yS.release();
+  ctx->alm_wZ.release();
+  if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->d_scal) cudaFree(ctx->d_scal);
+  if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
+  if (ctx->d_flag) cudaFree(ctx->d_flag);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char *drsdp_last_error(const drsdp_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int drsdp_sync(drsdp_ctx *ctx) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "stream sync");
+}
+
+int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count) {
+  if (!ctx || !count) return DRSDP_ERR_INVALID_ARG;
+  *count = ctx->launches;
+  return DRSDP_OK;
+}
+
+int drsdp_set_problem(drsdp_ctx *ctx, int64_t n, int64_t m, const double *C, int64_t nnz, const int32_t *row,
+                      const int32_t *col, const int32_t *cons, const double *b) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (n <= 0 || n >= 65536 || m <= 0 || nnz < 0 || !b || (nnz > 0 && (!row || !col || !cons)))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_problem: bad sizes or NULL arrays");
+  cudaSetDevice(ctx->device);
+  Problem &P = ctx->prob;
+  P = Problem();
+  P.n = n;
+  P.m = m;
+  P.h_amap.assign((size_t)n * n, -1);
+  for (int64_t k = 0; k < nnz; ++k) {
+    const int32_t i = row[k], j = col[k], a = cons[k];
+    if (i < 0 || j < 0 || i >= n || j >= n || i > j || a < 0 || a >= m)
+      return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_problem: triplet " + std::to_string(k) + " out of range");
+    if (P.h_amap[(size_t)i * n + j] != -1)
+      return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_problem: duplicate position " + std::to_string(k));
+    P.h_amap[(size_t)i * n + j] = a;
+    P.h_amap[(size_t)j * n + i] = a;
+  }
+  if (C) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = i + 1; j < n; ++j)
+        if (C[i * n + j] != C[j * n + i]) return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_problem: C not symmetric");
+  }
+  P.h_b.assign(b, b + m);
+  ctx->has_problem = false;
+  return finalize_problem(ctx, C);
+}
+
+int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (d < 1 || d > 360 || !Q || !c) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_bqp: need 1 <= d <= 360");
+  for (int i = 0; i < d; ++i)
+    for (int j = i + 1; j < d; ++j)
+      if (Q[i * d + j] != Q[j * d + i]) return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_bqp: Q not symmetric");
+  cudaSetDevice(ctx->device);
+  MonoRank mr(d);
+  Problem &P = ctx->prob;
+  P = Problem();
+  const int64_t n = 1 + d + (int64_t)d * (d - 1) / 2;
+  P.n = n;
+  P.m = mr.off[5];
+  // basis monomials, graded-lex: [], [i], [i,j]
+  std::vector<int> bs(n * 2, -1);
+  std::vector<int> bk(n, 0);
+  int64_t t = 1;
+  for (int i = 0; i < d; ++i, ++t) {
+    bs[2 * t] = i;
+    bk[t] = 1;
+  }
+  for (int i = 0; i < d; ++i)
+    for (int j = i + 1; j < d; ++j, ++t) {
+      bs[2 * t] = i;
+      bs[2 * t + 1] = j;
+      bk[t] = 2;
+    }
+  P.h_amap.assign((size_t)n * n, -1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i; j < n; ++j) {
+      // symmetric difference of two sorted sets of size <= 2
+      int a[4], k = 0;
+      int ia = 0, ja = 0;
+      const int *A = &bs[2 * i], *B = &bs[2 * j];
+      const int ka = bk[i], kb = bk[j];
+      while (ia < ka || ja < kb) {
+        if (ja >= kb || (ia < ka && A[ia] < B[ja])) a[k++] = A[ia++];
+        else if (ia >= ka || B[ja] < A[ia]) a[k++] = B[ja++];
+        else {
+          ++ia;
+          ++ja;
+        }
+      }
+      const int32_t id = (int32_t)mr.id(a, k);
+      P.h_amap[(size_t)i * n + j] = id;
+      P.h_amap[(size_t)j * n + i] = id;
+    }
+  P.h_b.assign(P.m, 0.0);
+  double tr = 0.0;
+  for (int i = 0; i < d; ++i) tr += Q[i * d + i];
+  P.h_b[0] = tr;
+  for (int i = 0; i < d; ++i) {
+    int a[1] = {i};
+    P.h_b[mr.id(a, 1)] = c[i];
+  }
+  for (int i = 0; i < d; ++i)
+    for (int j = i + 1; j < d; ++j) {
+      int a[2] = {i, j};
+      P.h_b[mr.id(a, 2)] = 2.0 * Q[i * d + j];
+    }
+  ctx->has_problem = false;
+  return finalize_problem(ctx, nullptr);
+}
+
+int drsdp_get_sizes(drsdp_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_upper) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "no problem set");
+  if (n) *n = ctx->prob.n;
+  if (m) *m = ctx->prob.m;
+  if (n_upper) *n_upper = ctx->prob.n_upper;
+  return DRSDP_OK;
+}
+
+int drsdp_export_index_map(drsdp_ctx *ctx, int32_t *amap, int64_t *seg_ptr, uint32_t *seg_pos) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "no problem set");
+  Problem &P = ctx->prob;
+  if (amap) std::memcpy(amap, P.h_amap.data(), sizeof(int32_t) * P.h_amap.size());
+  if (seg_ptr) std::memcpy(seg_ptr, P.h_seg_ptr.data(), sizeof(int64_t) * P.h_seg_ptr.size());
+  if (seg_pos) std::memcpy(seg_pos, P.h_seg_pos.data(), sizeof(uint32_t) * P.h_seg_pos.size());
+  return DRSDP_OK;
+}
+
+int drsdp_default_params(drsdp_params *o) {
+  if (!o) return DRSDP_ERR_INVALID_ARG;
+  std::memset(o, 0, sizeof(*o));
+  o->sigma0 = 1.0;
+  o->sigma_min = 1e-3;
+  o->sigma_max = 1e7;
+  o->gamma = 2.0;
+  o->tau1 = 0.1;
+  o->tau2 = 1.0;
+  o->tol = 1e-8;
+  o->eig_neg_tol = 1e-9;
+  o->rank_tol = 1e-6;
+  o->eps_scale = 1e-2;
+  o->eps_floor = 1e-12;
+  o->time_limit_s = 0.0;
+  o->p0 = 2;
+  o->max_outer = 300;
+  o->max_rtr = 500;
+  o->max_tcg = 0;
+  o->escape_max = 3;
+  o->mode = 0;
+  o->seed = 0;
+  return DRSDP_OK;
+}
+
+int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
+  if (!ctx || !prm) return DRSDP_ERR_INVALID_ARG;
+  const drsdp_params &q = *prm;
+  if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
+        q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= 64 && q.max_outer >= 1 && q.max_rtr >= 1 &&
+        q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
+  ctx->prm = q;
+  return DRSDP_OK;
+}
+
+int drsdp_set_initial_factor(drsdp_ctx *ctx, int32_t p, const double *Y0) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "set_initial_factor before set_problem");
+  if (p < 1 || p > 64 || !Y0) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_initial_factor: 1 <= p <= 64");
+  const int64_t n = ctx->prob.n;
+  ctx->h_Y0.assign(Y0, Y0 + (size_t)n * p);
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0;
+    for (int c = 0; c < p; ++c) s += ctx->h_Y0[i * p + c] * ctx->h_Y0[i * p + c];
+    if (!(s > 0)) return set_error(ctx, DRSDP_ERR_NUMERIC, "set_initial_factor: zero row");
+    const double inv = 1.0 / std::sqrt(s);
+    for (int c = 0; c < p; ++c) ctx->h_Y0[i * p + c] *= inv;
+  }
+  ctx->p0_given = p;
+  return DRSDP_OK;
+}
+
+int drsdp_set_subproblem_matrix(drsdp_ctx *ctx, int64_t n, const double *M_dev, int64_t ldm) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (n <= 0 || n > (1 << 30) || !M_dev || ldm < n || ((uintptr_t)M_dev & 7))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_subproblem_matrix: need n > 0, ldm >= n, 8B-aligned M");
+  cudaSetDevice(ctx->device);
+  ctx->sub_M = M_dev;
+  ctx->sub_n = n;
+  ctx->sub_ldm = ldm;
+  ctx->sub_cached_valid = false;
+  CK(ctx->sub_rho.ensure(n), "alloc rho");
+  int rc = ensure_red(ctx, 1184, 2);
+  if (rc) return rc;
+  KL(fro2_launch((int)n, M_dev, ldm, ctx->red_part.ptr, ctx->counters + C_FRO, ctx->d_scal + S_MM, ctx->stream),
+     "fro2");
+  // cost extra = [||M||^2, 0]
+  KL(combine_launch(ctx->d_scal + S_MM, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA, ctx->stream), "combine");
+  KL(combine_launch(nullptr, 0.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA + 1, ctx->stream), "combine");
+  return DRSDP_OK;
+}
+
+int drsdp_subproblem_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y_dev, const double *U_dev,
+                          double *cost_dev, double *egrad_dev, double *rgrad_dev, double *hvp_dev) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->sub_M) return set_error(ctx, DRSDP_ERR_STATE, "subproblem_eval before set_subproblem_matrix");
+  if (p < 1 || p > 64 || !Y_dev || (flags & ~3) || !flags)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval: need 1 <= p <= 64, flags in {1,2,3}");
+  if ((flags & DRSDP_EVAL_HVP) && (!U_dev || !hvp_dev))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval: HVP needs U and hvp");
+  if ((flags & DRSDP_EVAL_HVP) && !(flags & DRSDP_EVAL_COSTGRAD) &&
+      !(ctx->sub_cached_valid && ctx->sub_cached_Y == Y_dev && ctx->sub_cached_p == p))
+    return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y");
+  const int n = (int)ctx->sub_n;
+  int rc = eval_fixed(ctx, flags, n, p, ctx->sub_M, ctx->sub_ldm, Y_dev, p, U_dev, cost_dev, egrad_dev, rgrad_dev,
+                      hvp_dev, ctx->sub_G.ptr, ctx->sub_K.ptr, ctx->sub_rho.ptr, ctx->d_scal + S_EXTRA, false);
+  if (rc) return rc;
+  if (flags & DRSDP_EVAL_COSTGRAD) {
+    ctx->sub_cached_valid = true;
+    ctx->sub_cached_Y = Y_dev;
+    ctx->sub_cached_p = p;
+  }
+  return DRSDP_OK;
+}
+
+int drsdp_subproblem_eval_host(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y, const double *U,
+                               double *cost, double *egrad, double *rgrad, double *hvp) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->sub_M) return set_error(ctx, DRSDP_ERR_STATE, "subproblem_eval_host before set_subproblem_matrix");
+  if (p < 1 || p > 64 || !Y || (flags & ~3) || !flags || ((flags & DRSDP_EVAL_HVP) && !U))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval_host: bad arguments");
+  cudaSetDevice(ctx->device);
+  const size_t np = (size_t)ctx->sub_n * p;
+  static thread_local DBuf<double> buf;
+  CK(buf.ensure(5 * np + 8), "alloc host-eval buffers");
+  double *dY = buf.ptr, *dU = dY + np, *dE = dU + np, *dR = dE + np, *dH = dR + np, *dC = dH + np;
+  CK(cudaMemcpyAsync(dY, Y, np * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D Y");
+  if (flags & DRSDP_EVAL_HVP) CK(cudaMemcpyAsync(dU, U, np * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D U");
+  int rc = drsdp_subproblem_eval(ctx, flags | DRSDP_EVAL_COSTGRAD, p, dY, dU, dC, egrad ? dE : nullptr, dR,
+                                 (flags & DRSDP_EVAL_HVP) ? dH : nullptr);
+  if (rc) return rc;
+  if (cost) CK(cudaMemcpyAsync(cost, dC, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H cost");
+  if (egrad) CK(cudaMemcpyAsync(egrad, dE, np * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H egrad");
+  if (rgrad) CK(cudaMemcpyAsync(rgrad, dR, np * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H rgrad");
+  if (hvp && (flags & DRSDP_EVAL_HVP)) CK(cudaMemcpyAsync(hvp, dH, np * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H hvp");
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  ctx->sub_cached_valid = false;  // device scratch Y is not the caller's pointer
+  return DRSDP_OK;
+}
+
+int drsdp_assemble_M(drsdp_ctx *ctx, const double *y_dev, const double *T_dev, int64_t ldt, double sigma,
+                     double *M_dev, int64_t ldm) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "assemble_M before set_problem");
+  Problem &P = ctx->prob;
+  if (!y_dev || !T_dev || !M_dev || ldt < P.n || ldm < P.n || !(sigma > 0))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "assemble_M: bad arguments");
+  int rc = ensure_red(ctx, 1184, 2);
+  if (rc) return rc;
+  AssembleArgs as;
+  as.n = (int)P.n;
+  as.amap = P.amap.ptr;
+  as.ldmap = P.ld;
+  as.y = y_dev;
+  as.C = P.has_C ? P.C.ptr : nullptr;
+  as.ldc = P.ld;
+  as.T = T_dev;
+  as.ldt = ldt;
+  as.sigma = sigma;
+  as.M = M_dev;
+  as.ldm = ldm;
+  as.part = ctx->red_part.ptr;
+  as.counter = ctx->counters + C_ASM;
+  as.scal_out = ctx->d_scal + S_M0;
+  KL(assemble_launch(as, ctx->stream), "assemble kernel");
+  return DRSDP_OK;
+}
+
+int drsdp_y_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, double *y_dev) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "y_update before set_problem");
+  if (p < 1 || !Y_dev || !y_dev) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "y_update: bad arguments");
+  Problem &P = ctx->prob;
+  int rc = ensure_red(ctx, segsum_blocks(P.m, P.n_large), 2);
+  if (rc) return rc;
+  SegArgs s = seg_args(ctx, p, Y_dev, nullptr, p, y_dev);
+  KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
+  return DRSDP_OK;
+}
+
+int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const double *y_dev, double sigma,
+                      double *T_dev, int64_t ldt, double *z_dev, double *scalars_dev) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "dual_update before set_problem");
+  Problem &P = ctx->prob;
+  if (p < 1 || p > 64 || !Y_dev || !y_dev || !T_dev || ldt < P.n || !z_dev || !scalars_dev)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "dual_update: bad arguments");
+  const int n = (int)P.n;
+  int rc = ensure_red(ctx, dual_update_blocks(n), 3);
+  if (rc) return rc;
+  rc = ensure_workspace(ctx, n, p);
+  if (rc) return rc;
+  DualArgs da;
+  da.n = n;
+  da.p = p;
+  da.Y = Y_dev;
+  da.ldy = p;
+  da.amap = P.amap.ptr;
+  da.ldmap = P.ld;
+  da.y = y_dev;
+  da.C = P.has_C ? P.C.ptr : nullptr;
+  da.ldc = P.ld;
+  da.sigma = sigma;
+  da.T = T_dev;
+  da.ldt = ldt;
+  da.part = ctx->red_part.ptr;
+  da.counter = ctx->counters + C_DUAL;
+  da.scal_out = ctx->d_scal + S_DUAL;
+  KL(dual_update_launch(da, ctx->stream), "dual update kernel");
+  SymvArgs a = base_symv(ctx, n, p, T_dev, ldt);
+  a.V = Y_dev;
+  a.ldv = p;
+  a.Y = Y_dev;
+  a.ldy = p;
+  a.zout = z_dev;
+  a.scal_out = ctx->d_scal + S_ZSUM;
+  rc = run_symv(ctx, a, EPI_ROWDOT, false);
+  if (rc) return rc;
+  KL(vdot_launch(P.m, y_dev, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY, ctx->stream),
+     "vdot");
+  // scalars: [||R||, b^T y, <C,T> + sum z, ||T||^2]
+  KL(combine_launch(nullptr, 0, nullptr, 0, 0, scalars_dev, ctx->stream), "combine");
+  CK(cudaMemcpyAsync(ctx->h_scal + S_DUAL, ctx->d_scal + S_DUAL, 8 * 10, cudaMemcpyDeviceToHost, ctx->stream),
+     "read");
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  double h[4] = {std::sqrt(ctx->h_scal[S_DUAL]), ctx->h_scal[S_BY], ctx->h_scal[S_DUAL + 2] + ctx->h_scal[S_ZSUM],
+                 ctx->h_scal[S_DUAL + 1]};
+  CK(cudaMemcpyAsync(scalars_dev, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream), "write scalars");
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  return DRSDP_OK;
+}
+
+int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev, int64_t ldt, double sigma,
+                   const double *Y_dev, const double *U_dev, double *cost_dev, double *egrad_dev, double *rgrad_dev,
+                   double *hvp_dev) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "alm_eval before set_problem");
+  Problem &P = ctx->prob;
+  if (p < 1 || p > 64 || !Y_dev || !T_dev || ldt < P.n || !(sigma > 0) || (flags & ~3) || !flags)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: bad arguments");
+  if ((flags & DRSDP_EVAL_HVP) && (!U_dev || !hvp_dev))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: HVP needs U and hvp");
+  const int n = (int)P.n;
+  CK(ctx->alm_M.ensure((size_t)n * P.ld), "alloc M");
+  CK(ctx->alm_yS.ensure(P.m), "alloc yS");
+  CK(ctx->alm_wZ.ensure(P.m), "alloc wZ");
+  CK(ctx->sub_rho.ensure(n), "alloc rho");
+  int rc;
+  if (flags & DRSDP_EVAL_COSTGRAD) {
+    rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->sub_G.ptr,
+                      ctx->sub_rho.ptr, cost_dev, egrad_dev, rgrad_dev);
+    if (rc) return rc;
+    ctx->alm_cached_valid = true;
+    ctx->alm_cached_Y = Y_dev;
+    ctx->alm_cached_T = T_dev;
+    ctx->alm_cached_p = p;
+    ctx->alm_cached_sigma = sigma;
+  } else if (!(ctx->alm_cached_valid && ctx->alm_cached_Y == Y_dev && ctx->alm_cached_T == T_dev &&
+               ctx->alm_cached_p == p && ctx->alm_cached_sigma == sigma)) {
+    return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y, T, sigma");
+  }
+  if (flags & DRSDP_EVAL_HVP) {
+    rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->sub_G.ptr, ctx->sub_K.ptr, ctx->sub_rho.ptr,
+                 ctx->alm_wZ.ptr, hvp_dev);
+    if (rc) return rc;
+  }
+  return DRSDP_OK;
+}
+
+}  // extern "C"

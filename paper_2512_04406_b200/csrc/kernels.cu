@@ -1,0 +1,565 @@
+// kernels.cu — the ADMM operator kernels and the manifold vector kernels (sm_100a, fp64).
+//
+//  gram        G = Y^T Y, K = U^T Y + Y^T U, ||G||^2            (Eq. 4.7 terms)
+//  segsum      y(S) = (AA*)^{-1} A(Y Y^T + C) and A(Z)/cnt,  Z = Y U^T + U Y^T
+//              deterministic CSR segmented sum over the index map (north star (d))
+//  assemble    M = A*(y) - C - T/sigma, with ||C + T/sigma||^2 (north star (a))
+//  dual_update T <- T - sigma (A*(y) - Y Y^T - C), ||R||, ||T||^2, <C,T>  (Alg. 2 step 6)
+//  vector ops  tangent projection (Lemma 4.1), row-normalisation retraction, the tCG
+//              updates with fused inner products, escape padding (Thm 4.5), Y W.
+// All reductions are fixed-order (block partials + last-block sum): results are bit-identical
+// from run to run.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace drsdp {
+
+// ----------------------------------------------------------------------------------------------
+// Gram: G = Y^T Y (p x p), optional K = U^T Y + Y^T U; gg = ||G||_F^2
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *__restrict__ Y, int ldy,
+                                                   const double *__restrict__ U, int ldu, int rows_per_block,
+                                                   double *part, unsigned *counter, double *G, double *K,
+                                                   double *gg) {
+  extern __shared__ double sh[];
+  const int pp = p * p;
+  const int nval = U ? 2 * pp : pp;
+  double *ys = sh;                  // [32][p]
+  double *us = sh + 32 * p;         // [32][p]
+  double acc[32];                   // up to 32 entries per thread (nval <= 8192)
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+  const int r0 = blockIdx.x * rows_per_block, r1 = min(n, r0 + rows_per_block);
+  for (int c0 = r0; c0 < r1; c0 += 32) {
+    const int cn = min(32, r1 - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cn * p; t += blockDim.x) {
+      const int i = t / p, c = t - i * p;
+      ys[t] = Y[(size_t)(c0 + i) * ldy + c];
+      if (U) us[t] = U[(size_t)(c0 + i) * ldu + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int e = threadIdx.x + k * 256;
+      if (e < nval) {
+        const bool isK = e >= pp;
+        const int ee = isK ? e - pp : e;
+        const int a = ee / p, b = ee - a * p;
+        double s = acc[k];
+        if (!isK) {
+          for (int i = 0; i < cn; ++i) s = fma(ys[i * p + a], ys[i * p + b], s);
+        } else {
+          for (int i = 0; i < cn; ++i) s = fma(us[i * p + a], ys[i * p + b], fma(ys[i * p + a], us[i * p + b], s));
+        }
+        acc[k] = s;
+      }
+    }
+  }
+  double *mine = part + (size_t)blockIdx.x * nval;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int e = threadIdx.x + k * 256;
+    if (e < nval) mine[e] = acc[k];
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned ticket;
+  if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  __threadfence();
+  double g2 = 0.0;
+  for (int e = threadIdx.x; e < nval; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(part + (size_t)b * nval + e);
+    if (e < pp) {
+      G[e] = s;
+      g2 += s * s;
+    } else {
+      K[e - pp] = s;
+    }
+  }
+  __shared__ double scratch[64];
+  double v[1] = {g2};
+  block_sum<1>(v, scratch);
+  if (threadIdx.x == 0) {
+    if (gg) gg[0] = v[0];
+    *counter = 0u;
+  }
+}
+
+cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
+  const int nval = a.U ? 2 * a.p * a.p : a.p * a.p;
+  if (nval > 32 * 256) return cudaErrorInvalidValue;
+  int nb = (a.n + 255) / 256;
+  if (nb > a.max_blocks) nb = a.max_blocks;
+  if (nb < 1) nb = 1;
+  int rpb = (a.n + nb - 1) / nb;
+  nb = (a.n + rpb - 1) / rpb;
+  const size_t smem = (size_t)2 * 32 * a.p * 8;
+  gram_kernel<<<nb, 256, smem, st>>>(a.n, a.p, a.Y, a.ldy, a.U, a.ldu, rpb, a.part, a.counter, a.G, a.K, a.gg);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------------
+// Segmented sums over the index map. Upper positions (i <= j) of each constraint are stored
+// CSR (constraint-major, (i, j) sorted), packed (i << 16) | j. Ordered-position sums count an
+// off-diagonal upper position twice.
+//   MODE_Y: out[a] = (sum_pos w_ij <y_i, y_j> + cA[a]) / cnt[a],  scalar sum_a (..)^2 / cnt[a]
+//   MODE_Z: out[a] = (sum_pos w_ij (<y_i, u_j> + <u_i, y_j>)) / cnt[a]
+// Small segments: one thread each (blocks [0, nb_small)); large segments: one warp each.
+// ----------------------------------------------------------------------------------------------
+template <bool ZMODE>
+DRSDP_DEV double seg_pos_value(uint32_t pk, const double *__restrict__ Y, const double *__restrict__ U, int ld,
+                               int p) {
+  const int i = pk >> 16, j = pk & 0xffff;
+  const double *yi = Y + (size_t)i * ld, *yj = Y + (size_t)j * ld;
+  double s = 0.0;
+  if (!ZMODE) {
+    for (int c = 0; c < p; ++c) s = fma(__ldg(yi + c), __ldg(yj + c), s);
+  } else {
+    const double *ui = U + (size_t)i * ld, *uj = U + (size_t)j * ld;
+    for (int c = 0; c < p; ++c) s = fma(__ldg(yi + c), __ldg(uj + c), fma(__ldg(ui + c), __ldg(yj + c), s));
+  }
+  return (i == j) ? s : 2.0 * s;
+}
+
+template <bool ZMODE>
+__global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
+  __shared__ double scratch[64];
+  double sq = 0.0;
+  if ((int)blockIdx.x < a.nb_small) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < a.m && !a.is_large[s]) {
+      const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
+      double acc = 0.0;
+      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+      if (!ZMODE && a.cA) acc += a.cA[s];
+      a.out[s] = acc / (double)a.cnt[s];
+      if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
+    }
+  } else {
+    const int lane = threadIdx.x & 31;
+    const int64_t li = (int64_t)(blockIdx.x - a.nb_small) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (li < a.n_large) {
+      const int s = a.large_ids[li];
+      const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
+      double acc = 0.0;
+      for (int64_t k = b0 + lane; k < b1; k += 32) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (!ZMODE && a.cA) acc += a.cA[s];
+        a.out[s] = acc / (double)a.cnt[s];
+        if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
+      }
+    }
+  }
+  if (ZMODE) return;
+  double v[1] = {sq};
+  grid_sum<1>(v, a.part, a.counter, a.scal_out, scratch);
+}
+
+cudaError_t segsum_launch(const SegArgs &a0, bool zmode, cudaStream_t st) {
+  SegArgs a = a0;
+  a.nb_small = (int)((a.m + 255) / 256);
+  const int nb_large = (int)((a.n_large + 7) / 8);
+  const int nb = a.nb_small + nb_large;
+  if (zmode)
+    segsum_kernel<true><<<nb, 256, 0, st>>>(a);
+  else
+    segsum_kernel<false><<<nb, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+int segsum_blocks(int64_t m, int64_t n_large) { return (int)((m + 255) / 256 + (n_large + 7) / 8); }
+
+// ----------------------------------------------------------------------------------------------
+// Assembly M = A*(y) - C - T/sigma (north star (a)); padding columns [n, ldm) are zeroed.
+// scal_out[0] = ||C + T/sigma||_F^2 = ||M_0||^2 (the y-independent cost constant).
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) assemble_kernel(int n, const int32_t *__restrict__ amap, int64_t ldmap,
+                                                       const double *__restrict__ y, const double *__restrict__ C,
+                                                       int64_t ldc, const double *__restrict__ T, int64_t ldt,
+                                                       double inv_sigma, double *__restrict__ M, int64_t ldm,
+                                                       double *part, unsigned *counter, double *scal_out) {
+  __shared__ double scratch[64];
+  double s2 = 0.0;
+  const int64_t total = (int64_t)n * ldm;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldm, j = e - i * ldm;
+    double v = 0.0;
+    if (j < n) {
+      const int32_t id = __ldg(amap + i * ldmap + j);
+      const double m0 = (C ? __ldg(C + i * ldc + j) : 0.0) + __ldg(T + i * ldt + j) * inv_sigma;
+      v = (id >= 0 ? __ldg(y + id) : 0.0) - m0;
+      s2 = fma(m0, m0, s2);
+    }
+    M[e] = v;
+  }
+  double vv[1] = {s2};
+  grid_sum<1>(vv, part, counter, scal_out, scratch);
+}
+
+cudaError_t assemble_launch(const AssembleArgs &a, cudaStream_t st) {
+  assemble_kernel<<<a.blocks, 256, 0, st>>>(a.n, a.amap, a.ldmap, a.y, a.C, a.ldc, a.T, a.ldt, 1.0 / a.sigma,
+                                            a.M, a.ldm, a.part, a.counter, a.scal_out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------------
+// Dual update (Alg. 2 step 6): R_ij = y[amap_ij] - <y_i, y_j> - C_ij ; T_ij -= sigma R_ij.
+// 32x32 tiles, rows of Y for the tile staged in shared memory (p in chunks of 32).
+// scal_out = [||R||_F^2, ||T_new||_F^2, <C, T_new>]
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) dual_update_kernel(int n, int p, const double *__restrict__ Y, int ldy,
+                                                          const int32_t *__restrict__ amap, int64_t ldmap,
+                                                          const double *__restrict__ y, const double *__restrict__ C,
+                                                          int64_t ldc, double sigma, double *__restrict__ T,
+                                                          int64_t ldt, double *part, unsigned *counter,
+                                                          double *scal_out) {
+  __shared__ double yi_s[32][33], yj_s[32][33];
+  __shared__ double scratch[3 * 8];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 x 32
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < p; c0 += 32) {
+    const int cn = min(32, p - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+      const int rr = t >> 5, cc = t & 31;
+      yi_s[rr][cc] = (i0 + rr < n && cc < cn) ? Y[(size_t)(i0 + rr) * ldy + c0 + cc] : 0.0;
+      yj_s[rr][cc] = (j0 + rr < n && cc < cn) ? Y[(size_t)(j0 + rr) * ldy + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ii = ty + 8 * k;
+      double acc = s[k];
+      for (int c = 0; c < cn; ++c) acc = fma(yi_s[ii][c], yj_s[tx][c], acc);
+      s[k] = acc;
+    }
+  }
+  double r2 = 0.0, t2 = 0.0, ct = 0.0;
+  const int j = j0 + tx;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = i0 + ty + 8 * k;
+    if (i < n && j < n) {
+      const int32_t id = amap[(int64_t)i * ldmap + j];
+      const double cij = C ? C[(int64_t)i * ldc + j] : 0.0;
+      const double R = (id >= 0 ? y[id] : 0.0) - s[k] - cij;
+      const double tn = T[(int64_t)i * ldt + j] - sigma * R;
+      T[(int64_t)i * ldt + j] = tn;
+      r2 = fma(R, R, r2);
+      t2 = fma(tn, tn, t2);
+      ct = fma(cij, tn, ct);
+    }
+  }
+  double v[3] = {r2, t2, ct};
+  grid_sum<3>(v, part, counter, scal_out, scratch);
+}
+
+cudaError_t dual_update_launch(const DualArgs &a, cudaStream_t st) {
+  dim3 grid((a.n + 31) / 32, (a.n + 31) / 32);
+  dual_update_kernel<<<grid, 256, 0, st>>>(a.n, a.p, a.Y, a.ldy, a.amap, a.ldmap, a.y, a.C, a.ldc, a.sigma, a.T,
+                                           a.ldt, a.part, a.counter, a.scal_out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------------
+// Vector kernels on n x p row-major arrays (pitch ld). Warp per row, lanes over columns.
+// ----------------------------------------------------------------------------------------------
+#define ROW_LOOP_BEGIN                                                       \
+  const int lane = threadIdx.x & 31;                                       \
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); \
+  if (row < n) {
+#define ROW_LOOP_END }
+
+// dots[k] = <A_k, B_k> for up to 3 pairs
+__global__ void __launch_bounds__(256) dot3_kernel(int n, int p, int ld, const double *A0, const double *B0,
+                                                   const double *A1, const double *B1, const double *A2,
+                                                   const double *B2, double *part, unsigned *counter,
+                                                   double *out) {
+  __shared__ double scratch[3 * 8];
+  double v[3] = {0.0, 0.0, 0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  for (int c = lane; c < p; c += 32) {
+    if (A0) v[0] = fma(A0[o + c], B0[o + c], v[0]);
+    if (A1) v[1] = fma(A1[o + c], B1[o + c], v[1]);
+    if (A2) v[2] = fma(A2[o + c], B2[o + c], v[2]);
+  }
+  ROW_LOOP_END
+  grid_sum<3>(v, part, counter, out, scratch);
+}
+
+// out = V - rowdot(V, Y) Y ;  optional scalar <out, out>
+__global__ void __launch_bounds__(256) project_kernel(int n, int p, int ld, const double *Y, const double *V,
+                                                      double *out, double *part, unsigned *counter,
+                                                      double *dots) {
+  __shared__ double scratch[8];
+  double v[1] = {0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double d = 0.0;
+  for (int c = lane; c < p; c += 32) d = fma(V[o + c], Y[o + c], d);
+  d = warp_sum(d);
+  for (int c = lane; c < p; c += 32) {
+    const double x = V[o + c] - d * Y[o + c];
+    out[o + c] = x;
+    v[0] = fma(x, x, v[0]);
+  }
+  ROW_LOOP_END
+  if (dots) grid_sum<1>(v, part, counter, dots, scratch);
+}
+
+// out_row = (Y_row + t V_row) / ||Y_row + t V_row||; flag[0] = 1 if a norm <= 1e-14
+__global__ void __launch_bounds__(256) retract_kernel(int n, int p, int ld, const double *Y, const double *V,
+                                                      double t, double *out, int *flag) {
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double s = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double x = fma(t, V[o + c], Y[o + c]);
+    s = fma(x, x, s);
+  }
+  s = warp_sum(s);
+  const double nrm = sqrt(s);
+  if (nrm <= 1e-14) {
+    if (lane == 0) atomicExch(flag, 1);
+  } else {
+    const double inv = 1.0 / nrm;
+    for (int c = lane; c < p; c += 32) out[o + c] = fma(t, V[o + c], Y[o + c]) * inv;
+  }
+  ROW_LOOP_END
+}
+
+// tCG step: eo = e + a d ; ho = h + a hd ; ro = r + a hd (ro optional)
+// dots = [<eo, g>, <eo, ho>, <ro, ro>, <eo, eo>]
+__global__ void __launch_bounds__(256) tcg_step_kernel(int n, int p, int ld, double alpha, const double *e,
+                                                       const double *d, double *eo, const double *h,
+                                                       const double *hd, double *ho, const double *r, double *ro,
+                                                       const double *g, double *part, unsigned *counter,
+                                                       double *dots) {
+  __shared__ double scratch[4 * 8];
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  for (int c = lane; c < p; c += 32) {
+    const size_t k = o + c;
+    const double hdv = hd[k];
+    const double ev = fma(alpha, d[k], e[k]);
+    const double hv = fma(alpha, hdv, h[k]);
+    eo[k] = ev;
+    ho[k] = hv;
+    v[0] = fma(ev, g[k], v[0]);
+    v[1] = fma(ev, hv, v[1]);
+    v[3] = fma(ev, ev, v[3]);
+    if (ro) {
+      const double rv = fma(alpha, hdv, r[k]);
+      ro[k] = rv;
+      v[2] = fma(rv, rv, v[2]);
+    }
+  }
+  ROW_LOOP_END
+  grid_sum<4>(v, part, counter, dots, scratch);
+}
+
+// tCG new direction: d = P_Y(-r + beta d) in place; dots = [<d,d>]
+__global__ void __launch_bounds__(256) newdir_kernel(int n, int p, int ld, const double *Y, const double *r,
+                                                     double beta, double *d, double *part, unsigned *counter,
+                                                     double *dots) {
+  __shared__ double scratch[8];
+  double v[1] = {0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double s = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double x = fma(beta, d[o + c], -r[o + c]);
+    s = fma(x, Y[o + c], s);
+  }
+  s = warp_sum(s);
+  for (int c = lane; c < p; c += 32) {
+    const double x = fma(beta, d[o + c], -r[o + c]) - s * Y[o + c];
+    d[o + c] = x;
+    v[0] = fma(x, x, v[0]);
+  }
+  ROW_LOOP_END
+  grid_sum<1>(v, part, counter, dots, scratch);
+}
+
+// out[:, 0:p_out] from in (pitch ldi) : out = [in[:, 0:p_in] * scale_in  | 0 ]  then optional
+// escape columns V (n x dv, column k at Vcols + k*ldv_col, i.e. column-major as cuSOLVER returns)
+// placed at columns [vcol0, vcol0 + dv).
+__global__ void __launch_bounds__(256) repack_kernel(int n, int p_in, int ldi, const double *in, int p_out,
+                                                     int ldo, double *out, int vcol0, int dv, const double *Vcols,
+                                                     int64_t ldv_col) {
+  ROW_LOOP_BEGIN
+  for (int c = lane; c < ldo; c += 32) {
+    double x = 0.0;
+    if (in && c < p_in) x = in[(size_t)row * ldi + c];
+    if (Vcols && c >= vcol0 && c < vcol0 + dv) x = Vcols[(size_t)(c - vcol0) * ldv_col + row];
+    if (c >= p_out) x = 0.0;
+    out[(size_t)row * ldo + c] = x;
+  }
+  ROW_LOOP_END
+}
+
+// out = normalize_rows(Y W), W p x r (row-major), out pitch ldo (columns >= r zeroed)
+__global__ void __launch_bounds__(256) apply_w_kernel(int n, int p, int ld, const double *Y, const double *W,
+                                                      int r, int ldo, double *out) {
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double vals[8];
+  double s = 0.0;
+  // r <= 256 supported: lanes own columns lane + 32 h
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const int c = lane + 32 * h;
+    double x = 0.0;
+    if (c < r)
+      for (int k = 0; k < p; ++k) x = fma(Y[o + k], W[k * r + c], x);
+    vals[h] = x;
+    s = fma(x, x, s);
+  }
+  s = warp_sum(s);
+  const double inv = 1.0 / sqrt(s);
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    const int c = lane + 32 * h;
+    if (c < ldo) out[(size_t)row * ldo + c] = (c < r) ? vals[h] * inv : 0.0;
+  }
+  ROW_LOOP_END
+}
+
+// X (n x n, compact) = T - Diag(z)
+__global__ void __launch_bounds__(256) make_x_kernel(int n, const double *T, int64_t ldt, const double *z,
+                                                     double *X) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    double v = T[i * ldt + j];
+    if (i == j) v -= z[i];
+    X[e] = v;
+  }
+}
+
+// out[k] = sum_e a[e] * b[e] over length len vectors (k = 0), plus sum a^2 (k = 1)
+__global__ void __launch_bounds__(256) vdot_kernel(int64_t len, const double *a, const double *b, double *part,
+                                                   unsigned *counter, double *out) {
+  __shared__ double scratch[16];
+  double v[2] = {0.0, 0.0};
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a[e];
+    v[0] = fma(x, b ? b[e] : 0.0, v[0]);
+    v[1] = fma(x, x, v[1]);
+  }
+  grid_sum<2>(v, part, counter, out, scratch);
+}
+
+// D = A*(b / cnt) written into T (n x ldt); padding zeroed.
+__global__ void __launch_bounds__(256) init_d_kernel(int n, const int32_t *amap, int64_t ldmap, const double *b,
+                                                     const int32_t *cnt, double *T, int64_t ldt) {
+  const int64_t total = (int64_t)n * ldt;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldt, j = e - i * ldt;
+    double v = 0.0;
+    if (j < n) {
+      const int32_t id = amap[i * ldmap + j];
+      if (id >= 0) v = b[id] / (double)cnt[id];
+    }
+    T[e] = v;
+  }
+}
+
+// ||M||_F^2 over an n x n matrix with pitch ld
+__global__ void __launch_bounds__(256) fro2_kernel(int n, const double *M, int64_t ld, double *part,
+                                                   unsigned *counter, double *out) {
+  __shared__ double scratch[8];
+  double v[1] = {0.0};
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    const double x = __ldcs(M + i * ld + j);
+    v[0] = fma(x, x, v[0]);
+  }
+  grid_sum<1>(v, part, counter, out, scratch);
+}
+
+// scalars: out[0] = a[0] * s0 + b[0] * s1 + c  (tiny host-free combine)
+__global__ void combine_kernel(const double *a, double s0, const double *b, double s1, double c, double *out) {
+  if (threadIdx.x == 0) out[0] = (a ? a[0] * s0 : 0.0) + (b ? b[0] * s1 : 0.0) + c;
+}
+
+// ---------------------------------------------------------------------------------------------
+static inline int rows_grid(int64_t n) { return (int)((n + 7) / 8); }
+
+cudaError_t dot3_launch(int n, int p, int ld, const double *A0, const double *B0, const double *A1,
+                        const double *B1, const double *A2, const double *B2, double *part, unsigned *counter,
+                        double *out, cudaStream_t st) {
+  dot3_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, A0, B0, A1, B1, A2, B2, part, counter, out);
+  return cudaGetLastError();
+}
+cudaError_t project_launch(int n, int p, int ld, const double *Y, const double *V, double *out, double *part,
+                           unsigned *counter, double *dots, cudaStream_t st) {
+  project_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, V, out, part, counter, dots);
+  return cudaGetLastError();
+}
+cudaError_t retract_launch(int n, int p, int ld, const double *Y, const double *V, double t, double *out,
+                           int *flag, cudaStream_t st) {
+  retract_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, V, t, out, flag);
+  return cudaGetLastError();
+}
+cudaError_t tcg_step_launch(int n, int p, int ld, double alpha, const double *e, const double *d, double *eo,
+                            const double *h, const double *hd, double *ho, const double *r, double *ro,
+                            const double *g, double *part, unsigned *counter, double *dots, cudaStream_t st) {
+  tcg_step_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, alpha, e, d, eo, h, hd, ho, r, ro, g, part, counter,
+                                                dots);
+  return cudaGetLastError();
+}
+cudaError_t newdir_launch(int n, int p, int ld, const double *Y, const double *r, double beta, double *d,
+                          double *part, unsigned *counter, double *dots, cudaStream_t st) {
+  newdir_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, r, beta, d, part, counter, dots);
+  return cudaGetLastError();
+}
+cudaError_t repack_launch(int n, int p_in, int ldi, const double *in, int p_out, int ldo, double *out, int vcol0,
+                          int dv, const double *Vcols, int64_t ldv_col, cudaStream_t st) {
+  repack_kernel<<<rows_grid(n), 256, 0, st>>>(n, p_in, ldi, in, p_out, ldo, out, vcol0, dv, Vcols, ldv_col);
+  return cudaGetLastError();
+}
+cudaError_t apply_w_launch(int n, int p, int ld, const double *Y, const double *W, int r, int ldo, double *out,
+                           cudaStream_t st) {
+  if (r > 256) return cudaErrorInvalidValue;
+  apply_w_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, W, r, ldo, out);
+  return cudaGetLastError();
+}
+cudaError_t make_x_launch(int n, const double *T, int64_t ldt, const double *z, double *X, cudaStream_t st) {
+  make_x_kernel<<<1184, 256, 0, st>>>(n, T, ldt, z, X);
+  return cudaGetLastError();
+}
+cudaError_t vdot_launch(int64_t len, const double *a, const double *b, double *part, unsigned *counter,
+                        double *out, cudaStream_t st) {
+  int nb = (int)((len + 255) / 256);
+  if (nb > 592) nb = 592;
+  if (nb < 1) nb = 1;
+  vdot_kernel<<<nb, 256, 0, st>>>(len, a, b, part, counter, out);
+  return cudaGetLastError();
+}
+cudaError_t init_d_launch(int n, const int32_t *amap, int64_t ldmap, const double *b, const int32_t *cnt,
+                          double *T, int64_t ldt, cudaStream_t st) {
+  init_d_kernel<<<1184, 256, 0, st>>>(n, amap, ldmap, b, cnt, T, ldt);
+  return cudaGetLastError();
+}
+cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsigned *counter, double *out,
+                        cudaStream_t st) {
+  fro2_kernel<<<1184, 256, 0, st>>>(n, M, ld, part, counter, out);
+  return cudaGetLastError();
+}
+cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,
+                           cudaStream_t st) {
+  combine_kernel<<<1, 32, 0, st>>>(a, s0, b, s1, c, out);
+  return cudaGetLastError();
+}
+
+}  // namespace drsdp

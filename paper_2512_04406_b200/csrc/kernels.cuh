@@ -1,0 +1,104 @@
+// kernels.cuh — launchers of the operator and vector kernels (kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace drsdp {
+
+struct GramArgs {
+  int n = 0, p = 0;
+  const double *Y = nullptr;
+  int ldy = 0;
+  const double *U = nullptr;  // optional: K = U^T Y + Y^T U
+  int ldu = 0;
+  double *part = nullptr;  // >= max_blocks * 2 p^2
+  unsigned *counter = nullptr;
+  double *G = nullptr, *K = nullptr, *gg = nullptr;
+  int max_blocks = 296;
+};
+cudaError_t gram_launch(const GramArgs &a, cudaStream_t st);
+
+struct SegArgs {
+  int64_t m = 0;
+  const int64_t *seg_ptr = nullptr;
+  const uint32_t *seg_pos = nullptr;
+  const int32_t *cnt = nullptr;
+  const uint8_t *is_large = nullptr;
+  const int32_t *large_ids = nullptr;
+  int64_t n_large = 0;
+  const double *cA = nullptr;  // A(C) or nullptr
+  const double *Y = nullptr, *U = nullptr;
+  int ld = 0, p = 0;
+  double *out = nullptr;
+  double *part = nullptr;
+  unsigned *counter = nullptr;
+  double *scal_out = nullptr;  // MODE_Y: sum_a A(S+C)_a^2 / cnt_a
+  int nb_small = 0;
+};
+cudaError_t segsum_launch(const SegArgs &a, bool zmode, cudaStream_t st);
+int segsum_blocks(int64_t m, int64_t n_large);
+
+struct AssembleArgs {
+  int n = 0;
+  const int32_t *amap = nullptr;
+  int64_t ldmap = 0;
+  const double *y = nullptr, *C = nullptr;
+  int64_t ldc = 0;
+  const double *T = nullptr;
+  int64_t ldt = 0;
+  double sigma = 1.0;
+  double *M = nullptr;
+  int64_t ldm = 0;
+  double *part = nullptr;
+  unsigned *counter = nullptr;
+  double *scal_out = nullptr;
+  int blocks = 1184;
+};
+cudaError_t assemble_launch(const AssembleArgs &a, cudaStream_t st);
+
+struct DualArgs {
+  int n = 0, p = 0;
+  const double *Y = nullptr;
+  int ldy = 0;
+  const int32_t *amap = nullptr;
+  int64_t ldmap = 0;
+  const double *y = nullptr, *C = nullptr;
+  int64_t ldc = 0;
+  double sigma = 1.0;
+  double *T = nullptr;
+  int64_t ldt = 0;
+  double *part = nullptr;
+  unsigned *counter = nullptr;
+  double *scal_out = nullptr;  // [||R||^2, ||T||^2, <C,T>]
+};
+cudaError_t dual_update_launch(const DualArgs &a, cudaStream_t st);
+inline int dual_update_blocks(int n) { return ((n + 31) / 32) * ((n + 31) / 32); }
+
+cudaError_t dot3_launch(int n, int p, int ld, const double *A0, const double *B0, const double *A1,
+                        const double *B1, const double *A2, const double *B2, double *part, unsigned *counter,
+                        double *out, cudaStream_t st);
+cudaError_t project_launch(int n, int p, int ld, const double *Y, const double *V, double *out, double *part,
+                           unsigned *counter, double *dots, cudaStream_t st);
+cudaError_t retract_launch(int n, int p, int ld, const double *Y, const double *V, double t, double *out,
+                           int *flag, cudaStream_t st);
+cudaError_t tcg_step_launch(int n, int p, int ld, double alpha, const double *e, const double *d, double *eo,
+                            const double *h, const double *hd, double *ho, const double *r, double *ro,
+                            const double *g, double *part, unsigned *counter, double *dots, cudaStream_t st);
+cudaError_t newdir_launch(int n, int p, int ld, const double *Y, const double *r, double beta, double *d,
+                          double *part, unsigned *counter, double *dots, cudaStream_t st);
+cudaError_t repack_launch(int n, int p_in, int ldi, const double *in, int p_out, int ldo, double *out, int vcol0,
+                          int dv, const double *Vcols, int64_t ldv_col, cudaStream_t st);
+cudaError_t apply_w_launch(int n, int p, int ld, const double *Y, const double *W, int r, int ldo, double *out,
+                           cudaStream_t st);
+cudaError_t make_x_launch(int n, const double *T, int64_t ldt, const double *z, double *X, cudaStream_t st);
+cudaError_t vdot_launch(int64_t len, const double *a, const double *b, double *part, unsigned *counter,
+                        double *out, cudaStream_t st);
+cudaError_t init_d_launch(int n, const int32_t *amap, int64_t ldmap, const double *b, const int32_t *cnt,
+                          double *T, int64_t ldt, cudaStream_t st);
+cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsigned *counter, double *out,
+                        cudaStream_t st);
+cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,
+                           cudaStream_t st);
+inline int rows_blocks(int64_t n) { return (int)((n + 7) / 8); }
+
+}  // namespace drsdp

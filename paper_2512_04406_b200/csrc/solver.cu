@@ -1,0 +1,678 @@
+// solver.cu — Algorithm 2 (ManiDSDP) driven from the host: the ADMM/ALM outer
+// loop, the Riemannian trust-region inner solver with truncated CG, saddle escape
+// (Thm 4.5), rank adaptation (reading R15) and the sigma rule (Eq. 5.1).
+// All vector and matrix work runs in the device kernels on the context stream; the host reads
+// back a handful of scalars per tCG iteration. The eigen-decomposition of X (step 9, P:329,
+// and eta_d) uses cuSOLVER dsyevd (library call).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "kernels.cuh"
+#include "symv.cuh"
+
+namespace drsdp {
+
+#define CK(call, what)                       \
+  do {                                       \
+    int _rc = cuda_check(ctx, (call), what); \
+    if (_rc) return _rc;                     \
+  } while (0)
+#define KL(call, what)                       \
+  do {                                       \
+    ctx->launches++;                         \
+    int _rc = cuda_check(ctx, (call), what); \
+    if (_rc) return _rc;                     \
+  } while (0)
+#define RC(call)          \
+  do {                    \
+    int _rc = (call);     \
+    if (_rc) return _rc;  \
+  } while (0)
+
+struct Point {
+  double *Y = nullptr, *R = nullptr, *M = nullptr, *G = nullptr, *rho = nullptr, *yS = nullptr;
+  double f = 0.0, gn = 0.0;
+};
+
+struct SolverState {
+  int64_t n = 0, m = 0, ld = 0;
+  int ldp = 64;  // pitch of n x p vectors (p <= 64)
+  DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2];
+  DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
+  DBuf<double> T, X, W, ystar, z, Vst, Wsmall;
+  DBuf<int> devinfo;
+  DBuf<double> work;
+  cusolverDnHandle_t sol = nullptr;
+  Point cur, prop;
+  int p = 0;
+  bool have_solution = false;
+  double dual_obj = 0, primal_obj = 0;
+};
+
+void free_solver(drsdp_ctx *ctx) {
+  SolverState *s = ctx->solver;
+  if (!s) return;
+  for (int k = 0; k < 2; ++k) {
+    s->Ybuf[k].release();
+    s->Rbuf[k].release();
+    s->Mbuf[k].release();
+    s->Gbuf[k].release();
+    s->rhobuf[k].release();
+    s->ySbuf[k].release();
+  }
+  DBuf<double> *bs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw,
+                        &s->tmp, &s->K, &s->wZ, &s->T, &s->X, &s->W, &s->ystar, &s->z, &s->Vst, &s->Wsmall,
+                        &s->work};
+  for (auto *b : bs) b->release();
+  s->devinfo.release();
+  if (s->sol) cusolverDnDestroy(s->sol);
+  delete s;
+  ctx->solver = nullptr;
+}
+
+// cyclic Jacobi eigen-decomposition of a small symmetric matrix (host), ascending eigenvalues,
+// eigenvectors in columns of V (row-major p x p)
+static void jacobi_eig(int p, std::vector<double> A, std::vector<double> &w, std::vector<double> &V) {
+  V.assign((size_t)p * p, 0.0);
+  for (int i = 0; i < p; ++i) V[i * p + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < p; ++i)
+      for (int j = 0; j < p; ++j) {
+        tot += A[i * p + j] * A[i * p + j];
+        if (i != j) off += A[i * p + j] * A[i * p + j];
+      }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int i = 0; i < p; ++i)
+      for (int j = i + 1; j < p; ++j) {
+        const double aij = A[i * p + j];
+        if (aij == 0.0) continue;
+        const double th = (A[j * p + j] - A[i * p + i]) / (2.0 * aij);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < p; ++k) {
+          const double aki = A[k * p + i], akj = A[k * p + j];
+          A[k * p + i] = c * aki - s * akj;
+          A[k * p + j] = s * aki + c * akj;
+        }
+        for (int k = 0; k < p; ++k) {
+          const double aik = A[i * p + k], ajk = A[j * p + k];
+          A[i * p + k] = c * aik - s * ajk;
+          A[j * p + k] = s * aik + c * ajk;
+        }
+        for (int k = 0; k < p; ++k) {
+          const double vki = V[k * p + i], vkj = V[k * p + j];
+          V[k * p + i] = c * vki - s * vkj;
+          V[k * p + j] = s * vki + c * vkj;
+        }
+      }
+  }
+  std::vector<int> idx(p);
+  for (int i = 0; i < p; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return A[a * p + a] < A[b * p + b]; });
+  w.resize(p);
+  std::vector<double> V2((size_t)p * p);
+  for (int k = 0; k < p; ++k) {
+    w[k] = A[idx[k] * p + idx[k]];
+    for (int i = 0; i < p; ++i) V2[i * p + k] = V[i * p + idx[k]];
+  }
+  V.swap(V2);
+}
+
+static double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+struct Run {
+  drsdp_ctx *ctx;
+  SolverState *s;
+  const drsdp_params &prm;
+  int n;
+  double sigma = 1.0;
+  int64_t costgrad = 0, hvp = 0, rtr_total = 0, tcg_total = 0;
+
+  int costgrad_at(Point &P, int p) {
+    ++costgrad;
+    RC(alm_or_fixed_costgrad(P, p));
+    RC(read_scalars(ctx, S_COST, 4));
+    P.f = ctx->h_scal[S_COST];
+    P.gn = std::sqrt(std::max(0.0, ctx->h_scal[S_SCAL + 1]));
+    if (!std::isfinite(P.f) || !std::isfinite(P.gn)) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite cost");
+    return DRSDP_OK;
+  }
+  // fixed-M reading: M = A*(y^k) - C - T/sigma assembled once per outer iteration into s->X
+  bool fixed_mode() const { return prm.mode == 1; }
+  int alm_or_fixed_costgrad(Point &P, int p) {
+    if (!fixed_mode())
+      return alm_costgrad(ctx, p, s->T.ptr, s->ld, sigma, P.Y, s->ldp, P.M, s->ld, P.yS, P.G, P.rho,
+                          ctx->d_scal + S_COST, nullptr, P.R);
+    // fixed M lives in s->Mbuf[0] (never swapped in this mode); yS = y(S) for the outer update
+    RC(eval_fixed(ctx, DRSDP_EVAL_COSTGRAD, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, nullptr, ctx->d_scal + S_COST,
+                  nullptr, P.R, nullptr, P.G, nullptr, P.rho, ctx->d_scal + S_EXTRA, false));
+    return DRSDP_OK;
+  }
+  int hvp_at(Point &P, int p, const double *U, double *H) {
+    ++hvp;
+    if (!fixed_mode()) return alm_hvp(ctx, p, P.M, s->ld, P.Y, s->ldp, U, P.G, s->K.ptr, P.rho, s->wZ.ptr, H);
+    return eval_fixed(ctx, DRSDP_EVAL_HVP, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, U, nullptr, nullptr, nullptr, H,
+                      ctx->sub_G.ptr, s->K.ptr, P.rho, nullptr, true);
+  }
+  int dots(double *out3, const double *A0, const double *B0, const double *A1, const double *B1, const double *A2,
+           const double *B2, int p) {
+    KL(dot3_launch(n, p, s->ldp, A0, B0, A1, B1, A2, B2, ctx->red_part.ptr, ctx->counters + C_VEC,
+                   ctx->d_scal + S_DOTS, ctx->stream),
+       "dot3");
+    RC(read_scalars(ctx, S_DOTS, 3));
+    for (int k = 0; k < 3; ++k) out3[k] = ctx->h_scal[S_DOTS + k];
+    return DRSDP_OK;
+  }
+  void swap_pts() { std::swap(s->cur, s->prop); }
+
+  // Steihaug-Toint truncated CG (oracle/rtr.py tcg), device vectors, scalar decisions on host.
+  int tcg(int p, double Delta, int max_tcg, int &iters, bool &hit) {
+    Point &C = s->cur;
+    const size_t bytes = (size_t)n * s->ldp * 8;
+    CK(cudaMemsetAsync(s->eta.ptr, 0, bytes, ctx->stream), "memset");
+    CK(cudaMemsetAsync(s->Heta.ptr, 0, bytes, ctx->stream), "memset");
+    CK(cudaMemcpyAsync(s->r.ptr, C.R, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+    CK(cudaMemsetAsync(s->delta.ptr, 0, bytes, ctx->stream), "memset");
+    double r_r = C.gn * C.gn;
+    const double norm_r0 = C.gn;
+    KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, 0.0, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
+                     ctx->d_scal + S_DOTS, ctx->stream),
+       "newdir");
+    double e_Pe = 0.0, e_Pd = 0.0, d_Pd = r_r, model = 0.0;
+    hit = false;
+    iters = 0;
+    for (int j = 1; j <= max_tcg; ++j) {
+      iters = j;
+      RC(hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr));
+      RC(read_scalars(ctx, S_SCAL, 1));
+      const double d_Hd = ctx->h_scal[S_SCAL];
+      if (!std::isfinite(d_Hd)) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
+      const double alpha = d_Hd != 0.0 ? r_r / d_Hd : INFINITY;
+      const double e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd;
+      if (d_Hd <= 0 || e_Pe_new >= Delta * Delta) {
+        const double tau = (-e_Pd + std::sqrt(e_Pd * e_Pd + d_Pd * (Delta * Delta - e_Pe))) / d_Pd;
+        KL(tcg_step_launch(n, p, s->ldp, tau, s->eta.ptr, s->delta.ptr, s->eta2.ptr, s->Heta.ptr, s->Hdelta.ptr,
+                           s->Heta2.ptr, nullptr, nullptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
+                           ctx->d_scal + S_DOTS, ctx->stream),
+           "tcg_step");
+        std::swap(s->eta, s->eta2);
+        std::swap(s->Heta, s->Heta2);
+        hit = true;
+        break;
+      }
+      KL(tcg_step_launch(n, p, s->ldp, alpha, s->eta.ptr, s->delta.ptr, s->eta2.ptr, s->Heta.ptr, s->Hdelta.ptr,
+                         s->Heta2.ptr, s->r.ptr, s->r2.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
+                         ctx->d_scal + S_DOTS, ctx->stream),
+         "tcg_step");
+      RC(read_scalars(ctx, S_DOTS, 3));
+      const double new_model = ctx->h_scal[S_DOTS] + 0.5 * ctx->h_scal[S_DOTS + 1];
+      if (new_model >= model) break;  // no model decrease: keep the previous eta
+      std::swap(s->eta, s->eta2);
+      std::swap(s->Heta, s->Heta2);
+      std::swap(s->r, s->r2);
+      model = new_model;
+      e_Pe = e_Pe_new;
+      const double r_r_old = r_r;
+      r_r = ctx->h_scal[S_DOTS + 2];
+      if (std::sqrt(r_r) <= norm_r0 * std::min(norm_r0, 0.1)) break;  // theta = 1, kappa = 0.1
+      const double beta = r_r / r_r_old;
+      KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, beta, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
+                       ctx->d_scal + S_DOTS, ctx->stream),
+         "newdir");
+      e_Pd = beta * (e_Pd + alpha * d_Pd);
+      d_Pd = r_r + beta * beta * d_Pd;
+    }
+    return DRSDP_OK;
+  }
+
+  int retract_into(const double *Y, const double *V, double t, double *out, int p, bool &bad) {
+    CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream), "memset");
+    KL(retract_launch(n, p, s->ldp, Y, V, t, out, ctx->d_flag, ctx->stream), "retract");
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+    bad = flag != 0;
+    return DRSDP_OK;
+  }
+
+  // Riemannian trust region (oracle/rtr.py rtr); s->cur holds Y on entry, the result on exit.
+  int rtr(int p, double grad_tol, bool warm, int &iters_out, int &tcg_out) {
+    RC(costgrad_at(s->cur, p));
+    if (warm) {
+      double t = 1.0;
+      for (int h = 0; h < 25; ++h) {
+        bool bad = false;
+        RC(retract_into(s->cur.Y, s->Uw.ptr, t, s->prop.Y, p, bad));
+        if (!bad) {
+          RC(costgrad_at(s->prop, p));
+          if (s->prop.f < s->cur.f) {
+            swap_pts();
+            break;
+          }
+        }
+        t *= 0.5;
+      }
+    }
+    const double delta_bar = std::sqrt((double)n);
+    double Delta = delta_bar / 8.0;
+    const int max_tcg = prm.max_tcg > 0 ? prm.max_tcg : std::max(1, n * (p - 1));
+    iters_out = 0;
+    tcg_out = 0;
+    for (int it = 0; it < prm.max_rtr; ++it) {
+      if (s->cur.gn <= grad_tol) break;
+      ++iters_out;
+      int nin = 0;
+      bool hit = false;
+      RC(tcg(p, Delta, max_tcg, nin, hit));
+      tcg_out += nin;
+      double d3[3];
+      RC(dots(d3, s->cur.R, s->eta.ptr, s->eta.ptr, s->Heta.ptr, nullptr, nullptr, p));
+      bool bad = false;
+      RC(retract_into(s->cur.Y, s->eta.ptr, 1.0, s->prop.Y, p, bad));
+      if (bad) {
+        Delta /= 4.0;
+        continue;
+      }
+      RC(costgrad_at(s->prop, p));
+      double rhonum = s->cur.f - s->prop.f;
+      double rhoden = -d3[0] - 0.5 * d3[1];
+      const double reg = std::max(1.0, std::fabs(s->cur.f)) * 2.220446049250313e-16 * 1e3;
+      rhonum += reg;
+      rhoden += reg;
+      const double rho = rhonum / rhoden;
+      if (rho < 0.25)
+        Delta /= 4.0;
+      else if (rho > 0.75 && hit)
+        Delta = std::min(2.0 * Delta, delta_bar);
+      if (rhoden >= 0 && rho > 0.1) swap_pts();
+      if (Delta < 1e-300) break;
+    }
+    return DRSDP_OK;
+  }
+};
+
+static int alloc_solver(drsdp_ctx *ctx) {
+  if (!ctx->solver) ctx->solver = new SolverState();
+  SolverState *s = ctx->solver;
+  Problem &P = ctx->prob;
+  s->n = P.n;
+  s->m = P.m;
+  s->ld = P.ld;
+  s->ldp = 64;
+  const size_t nv = (size_t)P.n * s->ldp;
+  for (int k = 0; k < 2; ++k) {
+    CK(s->Ybuf[k].ensure(nv), "alloc");
+    CK(s->Rbuf[k].ensure(nv), "alloc");
+    CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
+    CK(s->Gbuf[k].ensure(64 * 64), "alloc");
+    CK(s->rhobuf[k].ensure(P.n), "alloc");
+    CK(s->ySbuf[k].ensure(P.m), "alloc");
+  }
+  DBuf<double> *vs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw, &s->tmp};
+  for (auto *b : vs) CK(b->ensure(nv), "alloc");
+  CK(s->K.ensure(64 * 64), "alloc");
+  CK(s->wZ.ensure(P.m), "alloc");
+  CK(s->T.ensure((size_t)P.n * P.ld), "alloc T");
+  CK(s->X.ensure((size_t)P.n * P.n), "alloc X");
+  CK(s->W.ensure(P.n), "alloc W");
+  CK(s->ystar.ensure(P.m), "alloc");
+  CK(s->z.ensure(P.n), "alloc");
+  CK(s->Vst.ensure((size_t)P.n * 64), "alloc");
+  CK(s->Wsmall.ensure(64 * 64), "alloc");
+  CK(s->devinfo.ensure(1), "alloc");
+  CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large),
+                                                     (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184}) *
+                              4 + 64),
+     "alloc red");
+  for (int k = 0; k < 2; ++k) {
+    Point &pt = k == 0 ? s->cur : s->prop;
+    pt.Y = s->Ybuf[k].ptr;
+    pt.R = s->Rbuf[k].ptr;
+    pt.M = s->Mbuf[k].ptr;
+    pt.G = s->Gbuf[k].ptr;
+    pt.rho = s->rhobuf[k].ptr;
+    pt.yS = s->ySbuf[k].ptr;
+  }
+  if (!s->sol) {
+    if (cusolverDnCreate(&s->sol) != CUSOLVER_STATUS_SUCCESS) return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnCreate");
+  }
+  cusolverDnSetStream(s->sol, ctx->stream);
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)P.n, s->X.ptr,
+                                  (int)P.n, s->W.ptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd_bufferSize");
+  CK(s->work.ensure((size_t)lwork + 1), "alloc eig workspace");
+  return DRSDP_OK;
+}
+
+// gaussian rows, normalised (splitmix64 + Box-Muller), used when no initial factor was given
+static void draw_initial(uint64_t seed, int64_t n, int p, std::vector<double> &Y) {
+  Y.assign((size_t)n * p, 0.0);
+  uint64_t st = seed * 0x9E3779B97F4A7C15ull + 0x1234567ull;
+  auto next = [&]() {
+    uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  for (size_t k = 0; k < Y.size(); ++k) {
+    const double u1 = ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = ((next() >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    Y[k] = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0;
+    for (int c = 0; c < p; ++c) s += Y[i * p + c] * Y[i * p + c];
+    s = 1.0 / std::sqrt(s);
+    for (int c = 0; c < p; ++c) Y[i * p + c] *= s;
+  }
+}
+
+}  // namespace drsdp
+
+using namespace drsdp;
+
+extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "solve before set_problem");
+  cudaSetDevice(ctx->device);
+  const double t0 = now_s();
+  RC(alloc_solver(ctx));
+  SolverState *s = ctx->solver;
+  Problem &P = ctx->prob;
+  const drsdp_params &prm = ctx->prm;
+  const int n = (int)P.n;
+  RC(ensure_workspace(ctx, n, 64));
+  Run run{ctx, s, prm, n};
+  run.sigma = prm.sigma0;
+  // Y^0
+  int p = ctx->p0_given ? ctx->p0_given : prm.p0;
+  std::vector<double> Y0;
+  if (ctx->p0_given)
+    Y0 = ctx->h_Y0;
+  else
+    draw_initial(prm.seed, n, p, Y0);
+  {
+    std::vector<double> pad((size_t)n * s->ldp, 0.0);
+    for (int i = 0; i < n; ++i) std::memcpy(&pad[(size_t)i * s->ldp], &Y0[(size_t)i * p], sizeof(double) * p);
+    CK(cudaMemcpyAsync(s->cur.Y, pad.data(), pad.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy Y0");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+  }
+  // T^0 = D = A*(b/cnt) (X~^0 = 0), y^0 = 0
+  KL(init_d_launch(n, P.amap.ptr, P.ld, P.b.ptr, P.cnt.ptr, s->T.ptr, P.ld, ctx->stream), "init D");
+  CK(cudaMemsetAsync(s->ystar.ptr, 0, sizeof(double) * P.m, ctx->stream), "memset y");
+  double b_norm = 0.0;
+  for (double v : P.h_b) b_norm += v * v;
+  b_norm = std::sqrt(b_norm);
+  double C_norm = 0.0;
+  if (P.has_C) {
+    // ||C||_F from the device copy via fro2
+    KL(fro2_launch(n, P.C.ptr, P.ld, ctx->red_part.ptr, ctx->counters + C_FRO, ctx->d_scal + S_MM, ctx->stream),
+       "fro2");
+    RC(read_scalars(ctx, S_MM, 1));
+    C_norm = std::sqrt(ctx->h_scal[S_MM]);
+  }
+  ctx->trace.clear();
+  bool warm = false;
+  double eta_prev = 1.0;
+  int p_max = p;
+  int status = DRSDP_ERR_NOT_CONVERGED;
+  double eta_p = 0, eta_d = 0, eta_g = 0, dobj = 0, pobj = 0;
+  int outer = 0;
+  std::vector<double> lam(n);
+  for (int k = 0; k < prm.max_outer; ++k) {
+    outer = k + 1;
+    if (prm.mode == 1) {
+      // fixed-M: M = A*(y^k) - C - T/sigma and ||M||^2 as the cost constant
+      AssembleArgs as;
+      as.n = n;
+      as.amap = P.amap.ptr;
+      as.ldmap = P.ld;
+      as.y = s->ystar.ptr;
+      as.C = P.has_C ? P.C.ptr : nullptr;
+      as.ldc = P.ld;
+      as.T = s->T.ptr;
+      as.ldt = P.ld;
+      as.sigma = run.sigma;
+      as.M = s->Mbuf[0].ptr;
+      as.ldm = P.ld;
+      as.part = ctx->red_part.ptr;
+      as.counter = ctx->counters + C_ASM;
+      as.scal_out = ctx->d_scal + S_M0;
+      KL(assemble_launch(as, ctx->stream), "assemble");
+      KL(fro2_launch(n, s->Mbuf[0].ptr, P.ld, ctx->red_part.ptr, ctx->counters + C_FRO, ctx->d_scal + S_EXTRA,
+                     ctx->stream),
+         "fro2");
+      KL(combine_launch(nullptr, 0, nullptr, 0, 0, ctx->d_scal + S_EXTRA + 1, ctx->stream), "combine");
+    }
+    const double eps_k = std::max(0.1 * std::min(1.0, eta_prev) * prm.eps_scale, prm.eps_floor);
+    const double grad_tol = 4.0 * eps_k / run.sigma;
+    int rtr_it = 0, tcg_it = 0;
+    RC(run.rtr(p, grad_tol, warm, rtr_it, tcg_it));
+    run.rtr_total += rtr_it;
+    run.tcg_total += tcg_it;
+    const double grad_paper = 0.5 * run.sigma * s->cur.gn;
+    // y^{k+1} = y(S^{k+1})
+    if (prm.mode == 1) {
+      SegArgs sg;
+      sg.m = P.m;
+      sg.seg_ptr = P.seg_ptr.ptr;
+      sg.seg_pos = P.seg_pos.ptr;
+      sg.cnt = P.cnt.ptr;
+      sg.is_large = P.is_large.ptr;
+      sg.large_ids = P.large_ids.ptr;
+      sg.n_large = P.n_large;
+      sg.cA = P.has_C ? P.cA.ptr : nullptr;
+      sg.Y = s->cur.Y;
+      sg.ld = s->ldp;
+      sg.p = p;
+      sg.out = s->ystar.ptr;
+      sg.part = ctx->red_part.ptr;
+      sg.counter = ctx->counters + C_SEG;
+      sg.scal_out = ctx->d_scal + S_SEGSQ;
+      KL(segsum_launch(sg, false, ctx->stream), "segsum");
+    } else {
+      CK(cudaMemcpyAsync(s->ystar.ptr, s->cur.yS, sizeof(double) * P.m, cudaMemcpyDeviceToDevice, ctx->stream),
+         "copy y");
+    }
+    // T <- T - sigma (A*(y) - S - C)
+    DualArgs da;
+    da.n = n;
+    da.p = p;
+    da.Y = s->cur.Y;
+    da.ldy = s->ldp;
+    da.amap = P.amap.ptr;
+    da.ldmap = P.ld;
+    da.y = s->ystar.ptr;
+    da.C = P.has_C ? P.C.ptr : nullptr;
+    da.ldc = P.ld;
+    da.sigma = run.sigma;
+    da.T = s->T.ptr;
+    da.ldt = P.ld;
+    da.part = ctx->red_part.ptr;
+    da.counter = ctx->counters + C_DUAL;
+    da.scal_out = ctx->d_scal + S_DUAL;
+    KL(dual_update_launch(da, ctx->stream), "dual update");
+    // z = rowdot(T Y, Y)
+    {
+      SymvArgs a;
+      a.A = s->T.ptr;
+      a.lda = P.ld;
+      a.n = n;
+      a.p = p;
+      a.V = s->cur.Y;
+      a.ldv = s->ldp;
+      a.Y = s->cur.Y;
+      a.ldy = s->ldp;
+      a.zout = s->z.ptr;
+      a.scal_out = ctx->d_scal + S_ZSUM;
+      a.part = ctx->symv_part.ptr;
+      a.tile_cnt = ctx->tile_cnt.ptr;
+      a.tile_scal = ctx->tile_scal.ptr;
+      a.glob_cnt = ctx->counters + C_SYMV;
+      const int bn = symv_bn(symv_pt(p), false);
+      const int S = choose_splits(ctx, n, bn);
+      a.rows_per_split = (((n + S - 1) / S + 63) / 64) * 64;
+      KL(symv_launch(a, EPI_ROWDOT, false, S, ctx->stream), "symv rowdot");
+    }
+    KL(vdot_launch(P.m, s->ystar.ptr, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY,
+                   ctx->stream),
+       "vdot");
+    // X = T - Diag(z) and its eigen-decomposition
+    KL(make_x_launch(n, s->T.ptr, P.ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
+    {
+      int lwork = (int)s->work.cap - 1;
+      if (cusolverDnDsyevd(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, s->X.ptr, n, s->W.ptr,
+                           s->work.ptr, lwork, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
+        return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd");
+      ctx->launches++;
+    }
+    CK(cudaMemcpyAsync(lam.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
+    RC(read_scalars(ctx, S_DUAL, 8));
+    const double R_norm = std::sqrt(std::max(0.0, ctx->h_scal[S_DUAL]));
+    const double CT = ctx->h_scal[S_DUAL + 2];
+    const double zsum = ctx->h_scal[S_ZSUM];
+    dobj = ctx->h_scal[S_BY];
+    pobj = CT + zsum;
+    eta_p = R_norm / (1.0 + C_norm);
+    eta_d = std::max(0.0, -lam[0]) / (1.0 + std::fabs(lam[n - 1]));
+    eta_g = std::fabs(dobj - pobj) / (1.0 + std::fabs(dobj) + std::fabs(pobj));
+    const double eta_max = std::max(eta_p, std::max(eta_d, eta_g));
+    double row[13] = {(double)(k + 1), eta_p, eta_d, eta_g, eta_max, pobj, dobj, run.sigma, (double)p,
+                      (double)rtr_it, (double)tcg_it, 0.0, 0.0};
+    if (eta_max <= prm.tol) {
+      status = DRSDP_OK;
+      row[12] = now_s() - t0;
+      ctx->trace.insert(ctx->trace.end(), row, row + 13);
+      break;
+    }
+    // escape directions: eigenvectors with lambda < -eig_neg_tol (1 + |lambda_max|)
+    const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
+    int dv = 0;
+    while (dv < prm.escape_max && dv < n && lam[dv] < thresh) ++dv;
+    // rank reduction (reading R15): compress Y to its numerical rank
+    {
+      std::vector<double> G((size_t)p * p);
+      CK(cudaMemcpyAsync(G.data(), s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToHost, ctx->stream), "read G");
+      CK(cudaStreamSynchronize(ctx->stream), "sync");
+      std::vector<double> w, V;
+      jacobi_eig(p, G, w, V);
+      int r = 0;
+      for (int i = 0; i < p; ++i)
+        if (w[i] > prm.rank_tol * prm.rank_tol * w[p - 1]) ++r;
+      r = std::max(1, r);
+      if (r < p) {
+        std::vector<double> Wr((size_t)p * r);
+        for (int i = 0; i < p; ++i)
+          for (int c = 0; c < r; ++c) Wr[(size_t)i * r + c] = V[(size_t)i * p + (p - r + c)];
+        CK(cudaMemcpyAsync(s->Wsmall.ptr, Wr.data(), Wr.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy W");
+        KL(apply_w_launch(n, p, s->ldp, s->cur.Y, s->Wsmall.ptr, r, s->ldp, s->tmp.ptr, ctx->stream), "apply W");
+        CK(cudaMemcpyAsync(s->cur.Y, s->tmp.ptr, (size_t)n * s->ldp * 8, cudaMemcpyDeviceToDevice, ctx->stream),
+           "copy");
+        p = r;
+      }
+    }
+    if (dv > 0 && p + dv > 64) dv = 64 - p;
+    if (dv > 0) {
+      // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]
+      std::vector<double> Vh((size_t)n * dv);
+      CK(cudaMemcpyAsync(Vh.data(), s->X.ptr, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
+         "read V");
+      CK(cudaStreamSynchronize(ctx->stream), "sync");
+      for (int c = 0; c < dv; ++c) {
+        int km = 0;
+        for (int i = 1; i < n; ++i)
+          if (std::fabs(Vh[(size_t)c * n + i]) > std::fabs(Vh[(size_t)c * n + km])) km = i;
+        if (Vh[(size_t)c * n + km] < 0)
+          for (int i = 0; i < n; ++i) Vh[(size_t)c * n + i] = -Vh[(size_t)c * n + i];
+      }
+      CK(cudaMemcpyAsync(s->Vst.ptr, Vh.data(), Vh.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy V");
+      KL(repack_launch(n, p, s->ldp, s->cur.Y, p + dv, s->ldp, s->tmp.ptr, 0, 0, nullptr, 0, ctx->stream), "repack");
+      CK(cudaMemcpyAsync(s->cur.Y, s->tmp.ptr, (size_t)n * s->ldp * 8, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
+      KL(repack_launch(n, 0, s->ldp, nullptr, p + dv, s->ldp, s->Uw.ptr, p, dv, s->Vst.ptr, n, ctx->stream),
+         "repack");
+      p += dv;
+      warm = true;
+    } else {
+      warm = false;
+    }
+    p_max = std::max(p_max, p);
+    // sigma update, Eq. 5.1
+    const double ratio = R_norm / (1.0 + b_norm);
+    double sig = run.sigma;
+    if (ratio < prm.tau1 * grad_paper)
+      sig = std::max(run.sigma / prm.gamma, prm.sigma_min);
+    else if (ratio > prm.tau2 * grad_paper)
+      sig = std::min(prm.gamma * run.sigma, prm.sigma_max);
+    row[11] = dv;
+    row[12] = now_s() - t0;
+    ctx->trace.insert(ctx->trace.end(), row, row + 13);
+    run.sigma = sig;
+    eta_prev = eta_max;
+    if (prm.time_limit_s > 0 && now_s() - t0 > prm.time_limit_s) break;
+  }
+  s->p = p;
+  s->have_solution = true;
+  s->dual_obj = dobj;
+  s->primal_obj = pobj;
+  if (info) {
+    info->status = status;
+    info->outer_iters = outer;
+    info->p_final = p;
+    info->p_max = p_max;
+    info->rtr_iters = run.rtr_total;
+    info->tcg_iters = run.tcg_total;
+    info->n_costgrad = run.costgrad;
+    info->n_hvp = run.hvp;
+    info->eta_p = eta_p;
+    info->eta_d = eta_d;
+    info->eta_g = eta_g;
+    info->dual_obj = dobj;
+    info->primal_obj = pobj;
+    info->seconds = now_s() - t0;
+  }
+  return status;
+}
+
+extern "C" int drsdp_get_solution(drsdp_ctx *ctx, double *y, double *Y, int32_t *p, double *z, double *X) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  SolverState *s = ctx->solver;
+  if (!s || !s->have_solution) return set_error(ctx, DRSDP_ERR_STATE, "no solution (call drsdp_solve first)");
+  const int64_t n = s->n;
+  if (p) *p = s->p;
+  if (y) CK(cudaMemcpyAsync(y, s->ystar.ptr, sizeof(double) * s->m, cudaMemcpyDeviceToHost, ctx->stream), "read y");
+  if (Y)
+    CK(cudaMemcpy2DAsync(Y, sizeof(double) * s->p, s->cur.Y, sizeof(double) * s->ldp, sizeof(double) * s->p, n,
+                         cudaMemcpyDeviceToHost, ctx->stream),
+       "read Y");
+  if (z) CK(cudaMemcpyAsync(z, s->z.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read z");
+  if (X) {
+    KL(make_x_launch((int)n, s->T.ptr, s->ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
+    CK(cudaMemcpyAsync(X, s->X.ptr, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream), "read X");
+  }
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  return DRSDP_OK;
+}
+
+extern "C" int drsdp_get_trace(drsdp_ctx *ctx, int32_t max_rows, double *rows, int32_t *n_rows) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  const int avail = (int)(ctx->trace.size() / 13);
+  if (n_rows) *n_rows = avail;
+  if (rows && max_rows > 0) std::memcpy(rows, ctx->trace.data(), sizeof(double) * 13 * std::min(avail, (int)max_rows));
+  return DRSDP_OK;
+}

@@ -1,0 +1,55 @@
+// symv.cuh — interface of the fused tall-skinny symmetric product kernels (symv.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace drsdp {
+
+enum Epi { EPI_RAW = 0, EPI_COSTGRAD = 1, EPI_HVP = 2, EPI_ROWDOT = 3 };
+
+struct SymvArgs {
+  // symmetric operand A (n x n, row pitch lda) and the right operand V (n x p, pitch ldv)
+  const double *A = nullptr;
+  int64_t lda = 0;
+  int n = 0, p = 0;
+  const double *V = nullptr;
+  int ldv = 0;
+  // optional gather-product: acc += sum_i w[amap[i, j]] X[i, :]  (ALM HVP projection term)
+  const int32_t *amap = nullptr;
+  int64_t ldm = 0;
+  const double *w = nullptr;
+  const double *X = nullptr;
+  int ldx = 0;
+  // split-K
+  int rows_per_split = 0;
+  double *part = nullptr;      // [ntiles][S][BN*PT]
+  unsigned *tile_cnt = nullptr;  // [ntiles], zero on entry, left zero
+  // epilogue inputs
+  const double *Y = nullptr;  // rows y_j (n x p, pitch ldy)
+  int ldy = 0;
+  const double *U = nullptr;  // rows u_j (HVP)
+  int ldu = 0;
+  const double *G = nullptr;    // p x p Y^T Y
+  const double *K = nullptr;    // p x p U^T Y + Y^T U (HVP)
+  const double *rho = nullptr;  // n, rowdot(E, Y) at the same Y (HVP)
+  // outputs
+  double *out = nullptr;  // RAW: P; COSTGRAD: R; HVP: H
+  int ldo = 0;
+  double *egrad = nullptr;  // COSTGRAD, optional
+  int lde = 0;
+  double *rho_out = nullptr;  // COSTGRAD, optional
+  double *zout = nullptr;     // ROWDOT
+  // scalars
+  double *tile_scal = nullptr;  // [ntiles][2]
+  unsigned *glob_cnt = nullptr;
+  double *scal_out = nullptr;  // [2]: COSTGRAD (s1, ||R||^2), HVP (<U,H>, 0), ROWDOT (sum z, 0)
+  const double *gg = nullptr;          // ||G||_F^2 (COSTGRAD)
+  const double *cost_extra = nullptr;  // [2] constant cost terms (COSTGRAD)
+  double *cost_out = nullptr;
+};
+
+int symv_pt(int p);               // padded width used by the kernels (8, 16, 32, 64)
+int symv_bn(int pt, bool gather);  // output rows per CTA
+cudaError_t symv_launch(const SymvArgs &a, int epi, bool gather, int S, cudaStream_t st);
+
+}  // namespace drsdp

@@ -1,0 +1,54 @@
+"""CPU-side checks of the boundary: libdrsdp.so builds, loads and exports every symbol that
+include/drsdp.h declares; without a GPU drsdp_create fails with DRSDP_ERR_CUDA (no fallback)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "drsdp.h")).read()
+    return sorted(set(re.findall(r"^(?:int|void|const char \*)\s*\*?(drsdp_\w+)\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2512_04406_b200 import abi, build
+
+    build.build()
+    lib = ctypes.CDLL(abi.lib_path())
+    names = _declared()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(abi.EXPORTED) == set(names)
+
+
+def test_no_device_means_error_not_fallback():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2512_04406_b200 import abi
+
+    with pytest.raises(abi.DrsdpError) as ei:
+        abi.Context(0)
+    assert ei.value.code == abi.ERR_CUDA
+
+
+def test_default_params_match_design():
+    from paper_2512_04406_b200 import abi
+
+    prm = abi.Context.default_params()
+    assert prm.tol == 1e-8 and prm.sigma0 == 1.0 and prm.gamma == 2.0 and prm.p0 == 2
+    assert prm.mode == 0 and prm.escape_max == 3 and prm.eig_neg_tol == 1e-9
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2512_04406_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cc")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle_", ""), f

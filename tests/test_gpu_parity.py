@@ -1,0 +1,325 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * index map and segment structure: bit-exact;
+  * every subproblem evaluation (cost, gradients, HVP): <= 1e-10 relative, measured normwise
+    against the scale of the summands (||4 M Y|| + ||4 Y G|| for gradients, ||G||^2 + ||M||^2 for
+    the cost), because fp64 reorderings differ by O(n eps) of the summands, not of the result;
+  * full solves: eta_max <= 1e-8 and objective within 1e-6 relative of the oracle.
+"""
+import numpy as np
+import pytest
+
+from inputs import bqp_instance, initial_factor, random_matrix, random_symmetric, random_unit_factor, sweep_factor, \
+    sweep_matrix_cpu, sweep_matrix_torch
+from oracle import admm, bqp
+from oracle import operators as ops
+from oracle import subproblem as sp
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2512_04406_b200 import abi, build
+
+    build.build()
+    c = abi.Context(0, 0)  # legacy default stream = torch's current stream
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64, device="cuda")
+
+
+def rel(a, b, scale):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / scale)
+
+
+def gpu_fixed(ctx, M_np, Y, U=None, ld_pad=0, flags=3):
+    from paper_2512_04406_b200 import abi
+
+    n, p = Y.shape
+    ld = n + ld_pad
+    Mfull = np.full((n, ld), np.nan) if ld_pad else np.empty((n, ld))
+    Mfull[:, :n] = M_np
+    Md = dev(Mfull)
+    ctx.set_subproblem_matrix(n, Md, ld)
+    Yd, Ud = dev(Y), (dev(U) if U is not None else None)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    E, R = torch.empty_like(Yd), torch.empty_like(Yd)
+    H = torch.empty_like(Yd) if U is not None else None
+    if flags == 3 or U is None:
+        ctx.subproblem_eval(abi.EVAL_COSTGRAD | (abi.EVAL_HVP if U is not None else 0), p, Yd, Ud, cost, E, R, H)
+    else:  # separate calls: COSTGRAD, then HVP reusing the cached Gram / rho
+        ctx.subproblem_eval(abi.EVAL_COSTGRAD, p, Yd, None, cost, E, R, None)
+        ctx.subproblem_eval(abi.EVAL_HVP, p, Yd, Ud, None, None, None, H)
+    torch.cuda.synchronize()
+    out = {"f": cost.item(), "E": E.cpu().numpy(), "R": R.cpu().numpy()}
+    if H is not None:
+        out["H"] = H.cpu().numpy()
+    return out
+
+
+def check_fixed(g, o, M, Y):
+    G = Y.T @ Y
+    sE = np.linalg.norm(4 * M @ Y) + np.linalg.norm(4 * Y @ G)
+    assert abs(g["f"] - o["f"]) <= TOL * (np.sum(G * G) + np.sum(M * M)), (g["f"], o["f"])
+    assert rel(g["E"], o["E"], sE) <= TOL
+    assert rel(g["R"], o["R"], sE) <= TOL
+    if "H" in o:
+        assert rel(g["H"], o["H"], sE + 1.0) <= TOL
+
+
+@pytest.mark.parametrize("n", [4, 37, 200, 1000])
+@pytest.mark.parametrize("p", [1, 3, 8, 13, 16, 29, 32, 40, 64])
+def test_fixed_eval_sweep_distribution(ctx, n, p):
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    g = gpu_fixed(ctx, M, Y, U)
+    o = sp.fixed_eval(M, Y, U)
+    check_fixed(g, o, M, Y)
+
+
+@pytest.mark.parametrize("n,p", [(333, 16), (129, 5)])
+def test_fixed_eval_padded_pitch_and_split_calls(ctx, n, p):
+    """ldm > n with NaN padding (must never be read) and HVP in a separate call."""
+    M = random_symmetric(n, 3)
+    Y = random_unit_factor(n, p, 4)
+    U = sp.project(Y, random_matrix(n, p, 5))
+    g = gpu_fixed(ctx, M, Y, U, ld_pad=6, flags=0)
+    o = sp.fixed_eval(M, Y, U)
+    check_fixed(g, o, M, Y)
+
+
+def test_fixed_eval_deterministic(ctx):
+    n, p = 3000, 16
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    a = gpu_fixed(ctx, M, Y, U)
+    b = gpu_fixed(ctx, M, Y, U)
+    assert a["f"] == b["f"]
+    for k in ("E", "R", "H"):
+        assert np.array_equal(a[k], b[k])
+
+
+def test_host_entry_point(ctx):
+    n, p = 500, 8
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    Md = dev(M)
+    ctx.set_subproblem_matrix(n, Md, n)
+    from paper_2512_04406_b200 import abi
+
+    g = ctx.subproblem_eval_host(abi.EVAL_COSTGRAD | abi.EVAL_HVP, Y, U, want_egrad=True)
+    check_fixed(g, sp.fixed_eval(M, Y, U), M, Y)
+
+
+@pytest.mark.parametrize("n,p", [(16384, 16), (32768, 16), (16384, 64)])
+def test_fixed_eval_full_size_sampled(ctx, n, p):
+    """BASELINE sweep sizes in the bench's launch configuration: sampled rows against the
+    oracle's row formulas; the cost at n = 16384 against the blocked plain definition."""
+    from paper_2512_04406_b200 import abi
+
+    Md = sweep_matrix_torch(n)
+    Y, U = sweep_factor(n, p)
+    ctx.set_subproblem_matrix(n, Md, n)
+    Yd, Ud = dev(Y), dev(U)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    E, R, H = torch.empty_like(Yd), torch.empty_like(Yd), torch.empty_like(Yd)
+    ctx.subproblem_eval(abi.EVAL_COSTGRAD | abi.EVAL_HVP, p, Yd, Ud, cost, E, R, H)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    rows = np.sort(np.concatenate([rng.choice(n, 48, replace=False), [0, n - 1]]))
+    Mr = Md[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    o = sp.fixed_rows(Mr, rows, Y, U)
+    G = Y.T @ Y
+    sE = np.linalg.norm(4 * Mr @ Y) + np.linalg.norm(4 * Y[rows] @ G)
+    for k, gk in (("E", E), ("R", R), ("H", H)):
+        assert rel(gk.cpu().numpy()[rows], o[k], sE) <= TOL, k
+    # symmetric input: M really is symmetric on the sampled rows
+    assert np.array_equal(Mr[:, rows], Mr[:, rows].T)
+    if n == 16384:
+        f = sp.fixed_cost_blocked(lambda i0, i1: Md[i0:i1].cpu().numpy(), Y, 2048)
+        scale = np.sum(G * G) + float(torch.sum(Md * Md).item())
+        assert abs(cost.item() - f) <= TOL * scale
+
+
+# ----------------------------------------------------------------------------------------------
+# index map, operators, ALM evaluations
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 10, 12, 40])
+def test_index_map_bit_exact(ctx, d):
+    Q, c = bqp_instance(d, 0)
+    amap, cnt, b = bqp.relax(Q, c)
+    ctx.set_bqp(Q, c)
+    n, m, nu = ctx.sizes()
+    assert (n, m) == (amap.shape[0], cnt.size)
+    g_amap, seg_ptr, seg_pos = ctx.export_index_map()
+    assert np.array_equal(g_amap, amap)
+    # segments: constraint-major, (i, j) sorted upper positions; rebuilt from the oracle's map
+    iu, ju = np.triu_indices(n)
+    ids = amap[iu, ju]
+    order = np.lexsort((ju, iu, ids))
+    assert np.array_equal(seg_pos, ((iu[order].astype(np.uint64) << np.uint64(16)) | ju[order].astype(np.uint64)).astype(np.uint32))
+    assert np.array_equal(seg_ptr, np.concatenate([[0], np.cumsum(np.bincount(ids, minlength=m))]))
+
+
+def test_general_problem_entry(ctx):
+    """drsdp_set_problem with COO triplets reproduces set_bqp's map; errors are reported."""
+    from paper_2512_04406_b200 import abi
+
+    Q, c = bqp_instance(4, 1)
+    amap, cnt, b = bqp.relax(Q, c)
+    n, m = amap.shape[0], cnt.size
+    iu, ju = np.triu_indices(n)
+    ctx.set_problem(n, m, None, iu, ju, amap[iu, ju], b)
+    g_amap, _, _ = ctx.export_index_map()
+    assert np.array_equal(g_amap, amap)
+    with pytest.raises(abi.DrsdpError) as e:
+        ctx.set_problem(n, m + 1, None, iu, ju, amap[iu, ju], np.append(b, 0))
+    assert e.value.code == abi.ERR_SINGULAR_AAT
+    with pytest.raises(abi.DrsdpError) as e:
+        ctx.set_problem(n, m, None, np.append(iu, 0), np.append(ju, 0), np.append(amap[iu, ju], 0), b)
+    assert e.value.code == abi.ERR_NOT_SYMMETRIC
+    with pytest.raises(abi.DrsdpError) as e:
+        ctx.set_problem(n, m, None, ju[ju > iu], iu[ju > iu], amap[ju[ju > iu], iu[ju > iu]], b)
+    assert e.value.code == abi.ERR_INVALID_ARG
+
+
+def _state(d, seed, sigma, p):
+    Q, c = bqp_instance(d, seed)
+    amap, cnt, b = bqp.relax(Q, c)
+    n, m = amap.shape[0], cnt.size
+    D = ops.D_matrix(amap, cnt, b)
+    Xt = random_symmetric(n, seed + 1, 0.3)
+    Xt = Xt - ops.At(amap, ops.A(amap, Xt, m) / cnt)  # A(X~) = 0 (Lemma 3.1)
+    T = Xt + D
+    Y = random_unit_factor(n, p, seed + 2)
+    U = sp.project(Y, random_matrix(n, p, seed + 3))
+    return Q, c, amap, cnt, b, T, Y, U
+
+
+@pytest.mark.parametrize("d,seed,sigma,p", [(3, 0, 1.0, 2), (5, 1, 3.0, 5), (10, 2, 10.0, 11), (12, 3, 0.5, 16),
+                                            (14, 4, 2.0, 33)])
+def test_alm_eval_parity(ctx, d, seed, sigma, p):
+    from paper_2512_04406_b200 import abi
+
+    Q, c, amap, cnt, b, T, Y, U = _state(d, seed, sigma, p)
+    n = amap.shape[0]
+    ctx.set_bqp(Q, c)
+    ld = n + (-n) % 64
+    Tpad = np.zeros((n, ld))
+    Tpad[:, :n] = T
+    Td, Yd, Ud = dev(Tpad), dev(Y), dev(U)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    E, R, H = torch.empty_like(Yd), torch.empty_like(Yd), torch.empty_like(Yd)
+    ctx.alm_eval(abi.EVAL_COSTGRAD | abi.EVAL_HVP, p, Td, ld, sigma, Yd, Ud, cost, E, R, H)
+    torch.cuda.synchronize()
+    o = sp.alm_eval(T, amap, cnt, None, sigma, Y, U)
+    G = Y.T @ Y
+    sE = np.linalg.norm(4 * o["M"] @ Y) + np.linalg.norm(4 * Y @ G)
+    m0 = np.sum((T / sigma) ** 2)
+    assert abs(cost.item() - o["f"]) <= TOL * (np.sum(G * G) + m0 + np.sum(o["y"] ** 2 * cnt))
+    assert rel(E.cpu().numpy(), o["E"], sE) <= TOL
+    assert rel(R.cpu().numpy(), o["R"], sE) <= TOL
+    sH = sE + np.linalg.norm(4 * ops.At(amap, ops.A(amap, Y @ U.T + U @ Y.T, cnt.size) / cnt) @ Y)
+    assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
+
+
+@pytest.mark.parametrize("d,p", [(6, 3), (12, 7)])
+def test_operator_kernels(ctx, d, p):
+    """(a) assembly, (d) y-update and dual update against the oracle's plain definitions."""
+    Q, c, amap, cnt, b, T, Y, U = _state(d, 5, 2.0, p)
+    n, m = amap.shape[0], cnt.size
+    ctx.set_bqp(Q, c)
+    sigma = 2.5
+    yv = random_matrix(m, 1, 9)[:, 0]
+    ld = n + 3
+    Td = dev(np.hstack([T, np.zeros((n, 3))]))
+    Md = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    ctx.assemble_M(dev(yv), Td, ld, sigma, Md, ld)
+    Yd = dev(Y)
+    ys = torch.zeros(m, dtype=torch.float64, device="cuda")
+    ctx.y_update(p, Yd, ys)
+    z = torch.zeros(n, dtype=torch.float64, device="cuda")
+    scal = torch.zeros(4, dtype=torch.float64, device="cuda")
+    ctx.dual_update(p, Yd, ys, sigma, Td, ld, z, scal)
+    torch.cuda.synchronize()
+    M_or = ops.At(amap, yv) - T / sigma
+    assert np.abs(Md.cpu().numpy()[:, :n] - M_or).max() <= 1e-14 * (1 + np.abs(M_or).max())
+    assert np.all(Md.cpu().numpy()[:, n:] == 0)
+    S = Y @ Y.T
+    y_or = ops.y_update(amap, cnt, S, None)
+    assert np.abs(ys.cpu().numpy() - y_or).max() <= 1e-13 * (1 + np.abs(y_or).max())
+    Rm = ops.At(amap, y_or) - S
+    T_or = T - sigma * Rm
+    assert np.abs(Td.cpu().numpy()[:, :n] - T_or).max() <= 1e-12 * (1 + np.abs(T_or).max())
+    z_or = sp.rowdot(T_or @ Y, Y)
+    assert np.abs(z.cpu().numpy() - z_or).max() <= 1e-11 * (1 + np.abs(z_or).max())
+    sc = scal.cpu().numpy()
+    assert abs(sc[0] - np.linalg.norm(Rm)) <= 1e-11 * (1 + np.linalg.norm(Rm))
+    assert abs(sc[1] - b @ y_or) <= 1e-11 * (1 + abs(b @ y_or))
+    assert abs(sc[2] - np.sum(z_or)) <= 1e-11 * (1 + abs(np.sum(z_or)))
+    assert abs(sc[3] - np.sum(T_or ** 2)) <= 1e-11 * (1 + np.sum(T_or ** 2))
+
+
+# ----------------------------------------------------------------------------------------------
+# full solves
+# ----------------------------------------------------------------------------------------------
+def _gpu_solve(ctx, Q, c, p0, seed, **kw):
+    ctx.set_bqp(Q, c)
+    prm = ctx.default_params(p0=p0, **kw)
+    ctx.set_params(prm)
+    n = 1 + Q.shape[0] + Q.shape[0] * (Q.shape[0] - 1) // 2
+    ctx.set_initial_factor(initial_factor(n, p0, seed))
+    info = ctx.solve()
+    return info, ctx.solution(), ctx.trace()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_solve_d10_against_oracle_and_brute_force(ctx, seed):
+    Q, c = bqp_instance(10, seed)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 2, seed)
+    assert info["status"] == 0, info
+    eta = max(info["eta_p"], info["eta_d"], info["eta_g"])
+    assert eta <= 1e-8
+    amap, cnt, b = bqp.relax(Q, c)
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2), initial_factor(amap.shape[0], 2, seed))
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+    assert info["dual_obj"] <= bqp.brute_force(Q, c)[0] + 1e-6
+    # residues recomputed by the oracle on the returned tuple (S, y, X) — T = X + Diag z
+    X = ctx.solution(want_X=True)["X"]
+    T = X + np.diag(sol["z"])
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], T)
+    assert res["eta_max"] <= 1e-8
+    assert np.abs(np.linalg.norm(sol["Y"], axis=1) - 1).max() <= 1e-12
+    assert len(tr) == info["outer_iters"]
+
+
+def test_solve_toy_q2(ctx):
+    info, sol, tr = _gpu_solve(ctx, np.array([[0.0, 1.0], [1.0, 0.0]]), np.zeros(2), 2, 0)
+    assert info["status"] == 0 and abs(info["dual_obj"] + 2.0) <= 1e-6
+
+
+def test_solve_d20_against_oracle(ctx):
+    Q, c = bqp_instance(20, 0)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 2, 0)
+    assert info["status"] == 0, info
+    amap, cnt, b = bqp.relax(Q, c)
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2), initial_factor(amap.shape[0], 2, 0))
+    assert o["status"] == "converged"
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+
+
+def test_solve_deterministic(ctx):
+    Q, c = bqp_instance(8, 3)
+    a = _gpu_solve(ctx, Q, c, 2, 3)
+    b = _gpu_solve(ctx, Q, c, 2, 3)
+    strip = lambda tr: [{k: v for k, v in r.items() if k != "time_s"} for r in tr]
+    assert strip(a[2]) == strip(b[2])
+    assert np.array_equal(a[1]["Y"], b[1]["Y"])
