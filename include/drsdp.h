@@ -215,6 +215,16 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
 /* Device kernel launches issued by this context since creation (for launch accounting). */
 int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count);
 
+/* Live per-kernel timing of the fused product kernel (symv.cu): when enabled, CUDA events are
+ * recorded on the context stream immediately before and after every launch. enable != 0 starts
+ * (and resets) the collection, 0 stops it. */
+int drsdp_profile_enable(drsdp_ctx *ctx, int enable);
+
+/* Total device milliseconds and launch count of the product kernel since profile_enable, for
+ * kind 0 = all launches, 1 = COSTGRAD epilogue, 2 = HVP epilogue, 3 = other (RAW/ROWDOT).
+ * Synchronizes the context stream. */
+int drsdp_profile_read(drsdp_ctx *ctx, int32_t kind, double *ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,12 +90,17 @@ def alm_M(T, amap, cnt, C, sigma, S):
 
 
 def alm_cost(T, amap, cnt, C, sigma, Y) -> float:
-    """f^(Y) = ||S + C + T/sigma||^2 - sum_a A(S + C)_a^2 / cnt_a."""
+    """f^(Y) = ||S + C + T/sigma||^2 - sum_a A(S + C)_a^2 / cnt_a, evaluated in the equivalent
+    form (||x||^2 - ||P_A x||^2 = ||(I - P_A) x||^2, P_A = A*(AA*)^{-1}A orthogonal)
+        f^ = ||S + C - A*(y(S))||^2 + (2/sigma) <T, S + C> + ||T||^2 / sigma^2
+    whose first term is summed from its (small) entries instead of as the difference of two
+    O(n^2) sums (reading R29: needed for the trust-region ratio near convergence)."""
     m = cnt.size
     S = Y @ Y.T
     SC = S if C is None else S + C
-    a = ops.A(amap, SC, m)
-    return float(np.sum((SC + T / sigma) ** 2) - np.sum(a * a / cnt))
+    yS = ops.A(amap, SC, m) / cnt
+    R = SC - ops.At(amap, yS)
+    return float(np.sum(R * R) + (2.0 / sigma) * np.sum(T * SC) + np.sum(T * T) / sigma ** 2)
 
 
 def alm_eval(T, amap, cnt, C, sigma, Y, U=None) -> dict:
@@ -201,7 +206,8 @@ class ALMProblem:
         S = Y @ Y.T
         SC = S if self.C is None else S + self.C
         a = ops.A(self.amap, SC, self.m)
-        f = float(np.sum((SC + self.T / self.sigma) ** 2) - np.sum(a * a / self.cnt))
+        Rs = SC - ops.At(self.amap, a / self.cnt)  # (I - P_A)(S + C), see alm_cost
+        f = float(np.sum(Rs * Rs) + (2.0 / self.sigma) * np.sum(self.T * SC) + np.sum(self.T * self.T) / self.sigma ** 2)
         M = ops.At(self.amap, a / self.cnt) - self.T / self.sigma
         if self.C is not None:
             M = M - self.C

@@ -24,7 +24,7 @@ EXPORTED = ("drsdp_create", "drsdp_destroy", "drsdp_last_error", "drsdp_sync", "
             "drsdp_set_params", "drsdp_set_initial_factor", "drsdp_solve", "drsdp_get_solution",
             "drsdp_get_trace", "drsdp_set_subproblem_matrix", "drsdp_subproblem_eval",
             "drsdp_subproblem_eval_host", "drsdp_assemble_M", "drsdp_y_update", "drsdp_dual_update",
-            "drsdp_alm_eval", "drsdp_launch_count")
+            "drsdp_alm_eval", "drsdp_launch_count", "drsdp_profile_enable", "drsdp_profile_read")
 
 
 class DrsdpError(RuntimeError):
@@ -90,6 +90,8 @@ def load_library():
         "drsdp_dual_update": (C.c_int, [vp, i32, dp, dp, C.c_double, dp, i64, dp, dp]),
         "drsdp_alm_eval": (C.c_int, [vp, i32, i32, dp, i64, C.c_double, dp, dp, dp, dp, dp, dp]),
         "drsdp_launch_count": (C.c_int, [vp, C.POINTER(i64)]),
+        "drsdp_profile_enable": (C.c_int, [vp, C.c_int]),
+        "drsdp_profile_read": (C.c_int, [vp, i32, C.POINTER(C.c_double), C.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -262,3 +264,11 @@ class Context:
         c = C.c_int64()
         self._check(self.lib.drsdp_launch_count(self.h, C.byref(c)))
         return c.value
+
+    def profile_enable(self, on=True):
+        return self._check(self.lib.drsdp_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self, kind=0):
+        ms, cnt = C.c_double(), C.c_int64()
+        self._check(self.lib.drsdp_profile_read(self.h, kind, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value

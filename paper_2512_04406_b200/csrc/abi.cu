@@ -124,13 +124,36 @@ static SymvArgs base_symv(drsdp_ctx *ctx, int n, int p, const double *A, int64_t
   return a;
 }
 
+static int prof_begin(drsdp_ctx *ctx, int kind) {
+  if (!ctx->prof_on) return DRSDP_OK;
+  if (ctx->prof_used == ctx->prof_events.size()) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a), "event create");
+    CK(cudaEventCreate(&b), "event create");
+    ctx->prof_events.push_back({a, b});
+    ctx->prof_kind.push_back(0);
+  }
+  ctx->prof_kind[ctx->prof_used] = kind;
+  CK(cudaEventRecord(ctx->prof_events[ctx->prof_used].first, ctx->stream), "event record");
+  return DRSDP_OK;
+}
+
+static int prof_end(drsdp_ctx *ctx) {
+  if (!ctx->prof_on) return DRSDP_OK;
+  CK(cudaEventRecord(ctx->prof_events[ctx->prof_used].second, ctx->stream), "event record");
+  ctx->prof_used++;
+  return DRSDP_OK;
+}
+
 static int run_symv(drsdp_ctx *ctx, SymvArgs &a, int epi, bool gather) {
   const int bn = symv_bn(symv_pt(a.p), gather);
   const int S = choose_splits(ctx, a.n, bn);
   const int per = (a.n + S - 1) / S;
   a.rows_per_split = ((per + 63) / 64) * 64;
+  int rc = prof_begin(ctx, epi == EPI_COSTGRAD ? 1 : epi == EPI_HVP ? 2 : 3);
+  if (rc) return rc;
   KL(symv_launch(a, epi, gather, S, ctx->stream), "symv kernel");
-  return DRSDP_OK;
+  return prof_end(ctx);
 }
 
 // Fixed-M evaluation: cost/egrad/rgrad (COSTGRAD) and hvp (HVP), device pointers.
@@ -491,6 +514,11 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->alm_M.release();
   ctx->alm_yS.release();
   ctx->alm_wZ.release();
+  ctx->host_stage.release();
+  for (auto &e : ctx->prof_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   if (ctx->counters) cudaFree(ctx->counters);
   if (ctx->d_scal) cudaFree(ctx->d_scal);
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
@@ -510,6 +538,33 @@ int drsdp_sync(drsdp_ctx *ctx) {
 int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count) {
   if (!ctx || !count) return DRSDP_ERR_INVALID_ARG;
   *count = ctx->launches;
+  return DRSDP_OK;
+}
+
+int drsdp_profile_enable(drsdp_ctx *ctx, int enable) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  ctx->prof_on = enable != 0;
+  ctx->prof_used = 0;
+  return DRSDP_OK;
+}
+
+int drsdp_profile_read(drsdp_ctx *ctx, int32_t kind, double *ms, int64_t *launches) {
+  if (!ctx || kind < 0 || kind > 3) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  CK(cudaStreamSynchronize(ctx->stream), "sync");
+  double tot = 0.0;
+  int64_t cnt = 0;
+  for (size_t k = 0; k < ctx->prof_used; ++k) {
+    if (kind != 0 && ctx->prof_kind[k] != kind) continue;
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, ctx->prof_events[k].first, ctx->prof_events[k].second), "event elapsed");
+    tot += t;
+    ++cnt;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = cnt;
   return DRSDP_OK;
 }
 
@@ -735,7 +790,7 @@ int drsdp_subproblem_eval_host(drsdp_ctx *ctx, int32_t flags, int32_t p, const d
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval_host: bad arguments");
   cudaSetDevice(ctx->device);
   const size_t np = (size_t)ctx->sub_n * p;
-  static thread_local DBuf<double> buf;
+  DBuf<double> &buf = ctx->host_stage;
   CK(buf.ensure(5 * np + 8), "alloc host-eval buffers");
   double *dY = buf.ptr, *dU = dY + np, *dE = dU + np, *dR = dE + np, *dH = dR + np, *dC = dH + np;
   CK(cudaMemcpyAsync(dY, Y, np * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D Y");

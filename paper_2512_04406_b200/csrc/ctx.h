@@ -126,6 +126,15 @@ struct drsdp_ctx {
   std::vector<double> h_Y0;
   int p0_given = 0;
 
+  // live kernel timing (drsdp_profile_*)
+  bool prof_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::vector<int> prof_kind;
+  size_t prof_used = 0;
+
+  // host-entry staging buffers
+  drsdp::DBuf<double> host_stage;
+
   // solver
   drsdp::SolverState *solver = nullptr;
   std::vector<double> trace;  // 13 per row

@@ -207,3 +207,19 @@ def test_fixed_subproblem_is_nearest_correlation_matrix():
     prob = sp.FixedMProblem(M)
     Y, info = rtr(prob, random_unit_factor(n, n, 3), RTRParams(n, n), 1e-10)
     assert abs(info["f"] - f_ncm) <= 1e-7 * (1 + f_ncm)
+
+
+def test_alm_cost_forms_agree():
+    """The accurate evaluation of f^ equals its defining expression
+    ||S + C + T/sigma||^2 - sum_a A(S+C)_a^2/cnt_a (up to rounding of the latter)."""
+    amap, cnt, b, D, Xt, T, sigma = _bqp_state(5, 4, sigma=7.0, lemma31=False)
+    n, m = amap.shape[0], cnt.size
+    C = random_symmetric(n, 77, 0.1)
+    for s in range(3):
+        Y = random_unit_factor(n, 4, 80 + s)
+        S = Y @ Y.T
+        a = ops.A(amap, S + C, m)
+        ref = np.sum((S + C + T / sigma) ** 2) - np.sum(a * a / cnt)
+        assert abs(sp.alm_cost(T, amap, cnt, C, sigma, Y) - ref) <= 1e-12 * np.sum((S + C + T / sigma) ** 2)
+        f, _, _ = sp.ALMProblem(T, amap, cnt, C, sigma).costgrad(Y)
+        assert f == sp.alm_cost(T, amap, cnt, C, sigma, Y) or abs(f - ref) <= 1e-12 * abs(ref)
