@@ -236,7 +236,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   const int n = (int)P.n;
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
-  rc = ensure_red(ctx, std::max<int64_t>(segsum_blocks(P.m, P.n_large), 1184), 4);
+  rc = ensure_red(ctx, std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large), (int64_t)assemble_alm_blocks(n), 1184}), 4);
   if (rc) return rc;
   rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
   if (rc) return rc;
@@ -256,20 +256,10 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   as.ldm = ldm;
   as.part = ctx->red_part.ptr;
   as.counter = ctx->counters + C_ASM;
-  as.scal_out = ctx->d_scal + S_M0;
-  KL(assemble_launch(as, ctx->stream), "assemble kernel");
-  // cost constants: ||M0||^2 + sum a^2/cnt - 2 yS.cA
-  if (P.has_C) {
-    KL(vdot_launch(P.m, yS, P.cA.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_YCA, ctx->stream),
-       "vdot");
-    KL(combine_launch(ctx->d_scal + S_SEGSQ, 1.0, ctx->d_scal + S_YCA, -2.0, 0.0, ctx->d_scal + S_EXTRA + 1,
-                      ctx->stream),
-       "combine");
-  } else {
-    KL(combine_launch(ctx->d_scal + S_SEGSQ, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA + 1, ctx->stream),
-       "combine");
-  }
-  KL(combine_launch(ctx->d_scal + S_M0, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA, ctx->stream), "combine");
+  as.scal_out = ctx->d_scal + S_ALM;
+  KL(assemble_alm_launch(as, p, Y, ldv, ctx->stream), "assemble (ALM) kernel");
+  // accurate cost f^ = sum R^2 + (2/sigma) <T, S + C> + ||T||^2/sigma^2 (reading R29)
+  KL(alm_cost_launch(ctx->d_scal + S_ALM, sigma, cost ? cost : ctx->d_scal + S_COST, ctx->stream), "alm cost");
   SymvArgs a = base_symv(ctx, n, p, Mout, ldm);
   a.V = Y;
   a.ldv = ldv;
@@ -283,8 +273,8 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   a.rho_out = rho;
   a.scal_out = ctx->d_scal + S_SCAL;
   a.gg = ctx->d_scal + S_GG;
-  a.cost_extra = ctx->d_scal + S_EXTRA;
-  a.cost_out = cost ? cost : ctx->d_scal + S_COST;
+  a.cost_extra = nullptr;
+  a.cost_out = nullptr;  // the cost comes from the assembly pass (accurate form)
   return run_symv(ctx, a, EPI_COSTGRAD, false);
 }
 

@@ -53,6 +53,7 @@ enum Slot {
   S_ZSUM = 20,     // 2: sum z
   S_BY = 22,       // 2: b^T y, ||y||^2
   S_YCA = 24,      // 2: yS . cA
+  S_ALM = 26,      // 3: ALM assembly sums [sum R^2, <T, S+C>, ||T||^2]
   S_FLAG = 30,     // retraction flag (int stored in a double slot)
   S_TOTAL = 64
 };

@@ -208,6 +208,102 @@ cudaError_t assemble_launch(const AssembleArgs &a, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------------------------------
+// ALM assembly with the accurate cost (y-eliminated subproblem, reading R29):
+//   S_ij = <y_i, y_j>,  M_ij = y(S)[amap_ij] - C_ij - T_ij/sigma   (written, symmetric, mirrored)
+//   R_ij = S_ij + C_ij - y(S)[amap_ij]  ((I - P_A)(S + C) entry)
+//   scal_out = [sum R^2, sum T (S + C), sum T^2]  so that
+//   f^ = sum R^2 + (2/sigma) <T, S + C> + ||T||^2 / sigma^2.
+// Upper 32x32 tiles only (T, C, amap, M symmetric); an off-diagonal tile is mirrored through
+// shared memory and counted twice in the sums.
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) assemble_alm_kernel(int n, int p, const double *__restrict__ Y, int ldy,
+                                                           const int32_t *__restrict__ amap, int64_t ldmap,
+                                                           const double *__restrict__ y, const double *__restrict__ C,
+                                                           int64_t ldc, const double *__restrict__ T, int64_t ldt,
+                                                           double inv_sigma, double *__restrict__ M, int64_t ldm,
+                                                           double *part, unsigned *counter, double *scal_out) {
+  __shared__ double yi_s[32][33], yj_s[32][33];
+  __shared__ double mt[32][33];
+  __shared__ double scratch[3 * 8];
+  const int I = blockIdx.y, J = blockIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  if (I <= J) {
+    const int i0 = I * 32, j0 = J * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c0 = 0; c0 < p; c0 += 32) {
+      const int cn = min(32, p - c0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+        const int rr = t >> 5, cc = t & 31;
+        yi_s[rr][cc] = (i0 + rr < n && cc < cn) ? Y[(size_t)(i0 + rr) * ldy + c0 + cc] : 0.0;
+        yj_s[rr][cc] = (j0 + rr < n && cc < cn) ? Y[(size_t)(j0 + rr) * ldy + c0 + cc] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ii = ty + 8 * k;
+        double acc = s[k];
+        for (int c = 0; c < cn; ++c) acc = fma(yi_s[ii][c], yj_s[tx][c], acc);
+        s[k] = acc;
+      }
+    }
+    const double w = (I == J) ? 1.0 : 2.0;
+    const int j = j0 + tx;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ii = ty + 8 * k, i = i0 + ii;
+      double mval = 0.0;
+      if (i < n && j < n) {
+        const int32_t id = amap[(int64_t)i * ldmap + j];
+        const double ya = id >= 0 ? y[id] : 0.0;
+        const double cij = C ? C[(int64_t)i * ldc + j] : 0.0;
+        const double tij = T[(int64_t)i * ldt + j];
+        mval = ya - cij - tij * inv_sigma;
+        M[(int64_t)i * ldm + j] = mval;
+        const double sc = s[k] + cij;
+        const double R = sc - ya;
+        v[0] = fma(w * R, R, v[0]);
+        v[1] = fma(w * tij, sc, v[1]);
+        v[2] = fma(w * tij, tij, v[2]);
+      }
+      mt[ii][tx] = mval;
+    }
+    if (I != J) {
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int jj = ty + 8 * k;  // row of the mirrored tile = column jj of the tile
+        const int jr = j0 + jj, ic = i0 + tx;
+        if (jr < n && ic < n) M[(int64_t)jr * ldm + ic] = mt[tx][jj];
+      }
+    }
+  }
+  grid_sum<3>(v, part, counter, scal_out, scratch);
+}
+
+cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st) {
+  dim3 grid((a.n + 31) / 32, (a.n + 31) / 32);
+  assemble_alm_kernel<<<grid, 256, 0, st>>>(a.n, p, Y, ldy, a.amap, a.ldmap, a.y, a.C, a.ldc, a.T, a.ldt,
+                                            1.0 / a.sigma, a.M, a.ldm, a.part, a.counter, a.scal_out);
+  if (a.ldm > a.n) {
+    cudaError_t e = cudaMemset2DAsync(a.M + a.n, a.ldm * sizeof(double), 0, (a.ldm - a.n) * sizeof(double), a.n, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+// cost = s[0] + (2/sigma) s[1] + s[2] / sigma^2
+__global__ void alm_cost_kernel(const double *s, double inv_sigma, double *cost) {
+  if (threadIdx.x == 0) cost[0] = s[0] + 2.0 * inv_sigma * s[1] + s[2] * inv_sigma * inv_sigma;
+}
+
+cudaError_t alm_cost_launch(const double *s, double sigma, double *cost, cudaStream_t st) {
+  alm_cost_kernel<<<1, 32, 0, st>>>(s, 1.0 / sigma, cost);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------------------------
 // Dual update (Alg. 2 step 6): R_ij = y[amap_ij] - <y_i, y_j> - C_ij ; T_ij -= sigma R_ij.
 // 32x32 tiles, rows of Y for the tile staged in shared memory (p in chunks of 32).
 // scal_out = [||R||_F^2, ||T_new||_F^2, <C, T_new>]

@@ -55,6 +55,10 @@ struct AssembleArgs {
   int blocks = 1184;
 };
 cudaError_t assemble_launch(const AssembleArgs &a, cudaStream_t st);
+// tiled ALM assembly: M(S) plus [sum R^2, <T, S + C>, ||T||^2] in scal_out (3 doubles)
+cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st);
+cudaError_t alm_cost_launch(const double *s, double sigma, double *cost, cudaStream_t st);
+inline int assemble_alm_blocks(int n) { return ((n + 31) / 32) * ((n + 31) / 32); }
 
 struct DualArgs {
   int n = 0, p = 0;
