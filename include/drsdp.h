@@ -37,6 +37,11 @@ extern "C" {
 
 typedef struct drsdp_ctx drsdp_ctx; /* opaque; owns every device buffer it allocates */
 
+/* Largest factor width p accepted anywhere (evaluations, initial factor, solver rank growth).
+ * p <= 64 runs the fused single-pass kernels; 64 < p <= DRSDP_MAX_P runs the product kernel in
+ * column chunks of 64 followed by separate row-epilogue kernels (same arithmetic). */
+#define DRSDP_MAX_P 1024
+
 typedef enum {
   DRSDP_OK = 0,
   DRSDP_ERR_INVALID_ARG = 1,   /* NULL where not allowed, n <= 0, p < 1, id out of range, bad sizes */
@@ -174,7 +179,7 @@ enum { DRSDP_EVAL_COSTGRAD = 1, DRSDP_EVAL_HVP = 2 };
  * Riemannian Hessian. flags: COSTGRAD computes cost/egrad/rgrad (any output pointer may be NULL);
  * HVP computes hvp and needs U_dev; HVP without COSTGRAD in the same call reuses the Gram matrix
  * and rowdot(E, Y) cached by the last COSTGRAD call at the same Y_dev and p (else ERR_STATE).
- * 1 <= p <= 64. */
+ * 1 <= p <= DRSDP_MAX_P. */
 int drsdp_subproblem_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y_dev,
                           const double *U_dev, double *cost_dev, double *egrad_dev,
                           double *rgrad_dev, double *hvp_dev);

@@ -45,16 +45,20 @@ int cuda_check(drsdp_ctx *ctx, cudaError_t e, const char *what) {
     if (_rc) return _rc;                                      \
   } while (0)
 
-int choose_splits(drsdp_ctx *ctx, int n, int bn) {
-  const int ntiles = (n + bn - 1) / bn;
+static int prof_begin(drsdp_ctx *ctx, int kind);
+static int prof_end(drsdp_ctx *ctx);
+
+// split-K factor for a product with krows contraction rows and ntiles output tiles (all chunks):
+// rows per split are a multiple of 64 (4 rows x 8 warps x unroll 2); cost model = waves x rows.
+int choose_splits(drsdp_ctx *ctx, int krows, int ntiles) {
   const int slots = ctx->num_sms * 2;
   int bestS = 1;
   double best = 1e300;
   for (int S = 1; S <= 64; ++S) {
-    const int per = (n + S - 1) / S;
+    const int per = (krows + S - 1) / S;
     const int rps = ((per + 63) / 64) * 64;
     if (S > 1 && rps < 64) break;
-    if ((int64_t)(S - 1) * rps >= n) break;  // empty splits
+    if ((int64_t)(S - 1) * rps >= krows) break;  // empty splits
     const int ctas = ntiles * S;
     const int waves = (ctas + slots - 1) / slots;
     const double cost = (double)waves * (rps + 32) + 16.0 * S;
@@ -67,16 +71,33 @@ int choose_splits(drsdp_ctx *ctx, int n, int bn) {
 }
 
 int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
-  const int pt = symv_pt(p);
-  // symv split partials: ntiles * S * BN * PT = ~n * S * PT (S <= 64)
-  const int bn_min = 8;
-  const int64_t ntiles = (n + bn_min - 1) / bn_min + 1;
-  const size_t symv_need = (size_t)(n + 64) * 64 * pt;
-  CK(ctx->symv_part.ensure(symv_need), "alloc symv workspace");
-  CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
-  CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
+  (void)n;
+  (void)p;
   CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64), "alloc gram workspace");
   return DRSDP_OK;
+}
+
+// One launch of the product kernel family (symv.cu): sizes the split-K factor, grows the split
+// workspace / tile counters on demand and records the live timing events (kind 1..3) if enabled.
+int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind) {
+  const int pt = symv_pt(a.p);
+  const int bn = symv_bn(pt, mode2);
+  const int kext = a.k > 0 ? a.k : a.n;
+  const int ntiles = ((a.n + bn - 1) / bn) * symv_chunks(a.p, epi);
+  const int S = choose_splits(ctx, kext, ntiles);
+  const int per = (kext + S - 1) / S;
+  a.rows_per_split = ((per + 63) / 64) * 64;
+  if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bn * pt), "alloc split workspace");
+  CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
+  CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
+  a.part = ctx->symv_part.ptr;
+  a.tile_cnt = ctx->tile_cnt.ptr;
+  a.tile_scal = ctx->tile_scal.ptr;
+  a.glob_cnt = ctx->counters + C_SYMV;
+  int rc = prof_kind ? prof_begin(ctx, prof_kind) : DRSDP_OK;
+  if (rc) return rc;
+  KL(symv_launch(a, epi, mode2, atr, S, ctx->stream), "product kernel");
+  return prof_kind ? prof_end(ctx) : DRSDP_OK;
 }
 
 static int ensure_red(drsdp_ctx *ctx, int64_t blocks, int k) {
@@ -117,10 +138,6 @@ static SymvArgs base_symv(drsdp_ctx *ctx, int n, int p, const double *A, int64_t
   a.lda = lda;
   a.n = n;
   a.p = p;
-  a.part = ctx->symv_part.ptr;
-  a.tile_cnt = ctx->tile_cnt.ptr;
-  a.tile_scal = ctx->tile_scal.ptr;
-  a.glob_cnt = ctx->counters + C_SYMV;
   return a;
 }
 
@@ -146,14 +163,155 @@ static int prof_end(drsdp_ctx *ctx) {
 }
 
 static int run_symv(drsdp_ctx *ctx, SymvArgs &a, int epi, bool gather) {
-  const int bn = symv_bn(symv_pt(a.p), gather);
-  const int S = choose_splits(ctx, a.n, bn);
-  const int per = (a.n + S - 1) / S;
-  a.rows_per_split = ((per + 63) / 64) * 64;
-  int rc = prof_begin(ctx, epi == EPI_COSTGRAD ? 1 : epi == EPI_HVP ? 2 : 3);
+  return run_product(ctx, a, epi, gather ? MODE2_GATHER : MODE2_NONE, false,
+                     epi == EPI_COSTGRAD ? 1 : epi == EPI_HVP ? 2 : 3);
+}
+
+// ---- generic-p building blocks (p > 64: column-chunked RAW products + row epilogues) ----------
+// G = Y^T Y (p x p, pitch p) and ||G||^2 -> gg; with U also K = U^T Y + Y^T U
+static int gram_generic(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const double *U, double *G,
+                        double *K, double *gg) {
+  if (G) {
+    SymvArgs a = base_symv(ctx, p, p, Y, ldv);
+    a.k = n;
+    a.V = Y;
+    a.ldv = ldv;
+    a.out = G;
+    a.ldo = p;
+    int rc = run_product(ctx, a, EPI_RAW, MODE2_NONE, false, 0);
+    if (rc) return rc;
+    if (gg) KL(fro2_launch(p, G, p, ctx->red_part.ptr, ctx->counters + C_FRO, gg, ctx->stream), "fro2 G");
+  }
+  if (U && K) {
+    SymvArgs a = base_symv(ctx, p, p, U, ldv);
+    a.k = n;
+    a.V = Y;
+    a.ldv = ldv;
+    a.A2 = Y;
+    a.lda2 = ldv;
+    a.V2 = U;
+    a.ldv2 = ldv;
+    a.out = K;
+    a.ldo = p;
+    return run_product(ctx, a, EPI_RAW, MODE2_PAIR, false, 0);
+  }
+  return DRSDP_OK;
+}
+
+// W = A1 B1 (+ A2 B2): n x p rows times p x p (pitch p)
+static int small_right(drsdp_ctx *ctx, int n, int p, const double *A1, int lda, const double *B1, const double *A2,
+                       const double *B2, double *W, int ldw) {
+  SymvArgs a = base_symv(ctx, n, p, A1, lda);
+  a.k = p;
+  a.V = B1;
+  a.ldv = p;
+  if (A2) {
+    a.A2 = A2;
+    a.lda2 = lda;
+    a.V2 = B2;
+    a.ldv2 = p;
+  }
+  a.out = W;
+  a.ldo = ldw;
+  return run_product(ctx, a, EPI_RAW, A2 ? MODE2_PAIR : MODE2_NONE, true, 0);
+}
+
+static int ensure_big(drsdp_ctx *ctx, int n, int ldv) {
+  CK(ctx->big_P.ensure((size_t)n * ldv), "alloc product buffer");
+  CK(ctx->big_W.ensure((size_t)n * ldv), "alloc product buffer");
+  return DRSDP_OK;
+}
+
+// generic cost+grad at Y given G (gg already in S_GG): P = M Y, W = Y G, row epilogue
+static int costgrad_generic(drsdp_ctx *ctx, int n, int p, const double *M, int64_t ldm, const double *Y, int ldv,
+                            const double *G, double *cost, double *egrad, double *rgrad, double *rho,
+                            const double *cost_extra_dev) {
+  int rc = ensure_big(ctx, n, ldv);
   if (rc) return rc;
-  KL(symv_launch(a, epi, gather, S, ctx->stream), "symv kernel");
-  return prof_end(ctx);
+  SymvArgs a = base_symv(ctx, n, p, M, ldm);
+  a.V = Y;
+  a.ldv = ldv;
+  a.out = ctx->big_P.ptr;
+  a.ldo = ldv;
+  rc = run_product(ctx, a, EPI_RAW, MODE2_NONE, false, 1);
+  if (rc) return rc;
+  rc = small_right(ctx, n, p, Y, ldv, G, nullptr, nullptr, ctx->big_W.ptr, ldv);
+  if (rc) return rc;
+  KL(rowepi_costgrad_launch(n, p, ctx->big_P.ptr, ldv, ctx->big_W.ptr, ldv, Y, ldv, rgrad, ldv, egrad, ldv, rho,
+                            ctx->red_part.ptr, ctx->counters + C_VEC, ctx->d_scal + S_SCAL, ctx->d_scal + S_GG,
+                            cost_extra_dev, cost, ctx->stream),
+     "row epilogue (cost+grad)");
+  return DRSDP_OK;
+}
+
+// generic HVP at Y along U given G, K: Q = M U (+ gather), W = U G + Y K, row epilogue
+static int hvp_generic(drsdp_ctx *ctx, int n, int p, const double *M, int64_t ldm, const double *Y, int ldv,
+                       const double *U, const double *G, const double *K, const double *rho, const int32_t *amap,
+                       int64_t ldmap, const double *w, double *hvp) {
+  int rc = ensure_big(ctx, n, ldv);
+  if (rc) return rc;
+  SymvArgs a = base_symv(ctx, n, p, M, ldm);
+  a.V = U;
+  a.ldv = ldv;
+  if (amap) {
+    a.amap = amap;
+    a.ldm = ldmap;
+    a.w = w;
+    a.X = Y;
+    a.ldx = ldv;
+  }
+  a.out = ctx->big_P.ptr;
+  a.ldo = ldv;
+  rc = run_product(ctx, a, EPI_RAW, amap ? MODE2_GATHER : MODE2_NONE, false, 2);
+  if (rc) return rc;
+  rc = small_right(ctx, n, p, U, ldv, G, Y, K, ctx->big_W.ptr, ldv);
+  if (rc) return rc;
+  KL(rowepi_hvp_launch(n, p, ctx->big_P.ptr, ldv, ctx->big_W.ptr, ldv, Y, ldv, U, ldv, rho, hvp, ldv,
+                       ctx->red_part.ptr, ctx->counters + C_VEC, ctx->d_scal + S_SCAL, ctx->stream),
+     "row epilogue (hvp)");
+  return DRSDP_OK;
+}
+
+// z = rowdot(T Y, Y), sum z -> zsum (any p)
+int rowdot_product(drsdp_ctx *ctx, int n, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z,
+                   double *zsum) {
+  if (p <= 64) {
+    SymvArgs a = base_symv(ctx, n, p, T, ldt);
+    a.V = Y;
+    a.ldv = ldv;
+    a.Y = Y;
+    a.ldy = ldv;
+    a.zout = z;
+    a.scal_out = zsum;
+    return run_product(ctx, a, EPI_ROWDOT, MODE2_NONE, false, 3);
+  }
+  int rc = ensure_big(ctx, n, ldv);
+  if (rc) return rc;
+  SymvArgs a = base_symv(ctx, n, p, T, ldt);
+  a.V = Y;
+  a.ldv = ldv;
+  a.out = ctx->big_P.ptr;
+  a.ldo = ldv;
+  rc = run_product(ctx, a, EPI_RAW, MODE2_NONE, false, 3);
+  if (rc) return rc;
+  KL(rowdot_launch(n, p, ctx->big_P.ptr, ldv, Y, ldv, z, ctx->red_part.ptr, ctx->counters + C_VEC, zsum, ctx->stream),
+     "rowdot");
+  return DRSDP_OK;
+}
+
+// out = normalize_rows(Y W), W p x r (pitch r); columns [r, ldo) of out zeroed
+int apply_w_product(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const double *W, int r, double *out,
+                    int ldo) {
+  SymvArgs a = base_symv(ctx, n, r, Y, ldv);
+  a.k = p;
+  a.V = W;
+  a.ldv = r;
+  a.out = out;
+  a.ldo = ldo;
+  int rc = run_product(ctx, a, EPI_RAW, MODE2_NONE, true, 0);
+  if (rc) return rc;
+  KL(normalize_rows_launch(n, r, ldo, out, ctx->stream), "normalize rows");
+  return DRSDP_OK;
 }
 
 // Fixed-M evaluation: cost/egrad/rgrad (COSTGRAD) and hvp (HVP), device pointers.
@@ -162,6 +320,22 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
                double *rho, const double *cost_extra_dev, bool have_gram) {
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
+  if (p > 64) {
+    if (flags & DRSDP_EVAL_COSTGRAD) {
+      rc = gram_generic(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
+      if (rc) return rc;
+      rc = costgrad_generic(ctx, n, p, M, ldm, Y, ldv, G, cost ? cost : ctx->d_scal + S_COST, egrad, rgrad, rho,
+                            cost_extra_dev);
+      if (rc) return rc;
+    }
+    if (flags & DRSDP_EVAL_HVP) {
+      rc = gram_generic(ctx, n, p, Y, ldv, U, G, K, nullptr);
+      if (rc) return rc;
+      rc = hvp_generic(ctx, n, p, M, ldm, Y, ldv, U, G, K, rho, nullptr, 0, nullptr, hvp);
+      if (rc) return rc;
+    }
+    return DRSDP_OK;
+  }
   if (flags & DRSDP_EVAL_COSTGRAD) {
     rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
     if (rc) return rc;
@@ -238,7 +412,8 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   if (rc) return rc;
   rc = ensure_red(ctx, std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large), (int64_t)assemble_alm_blocks(n), 1184}), 4);
   if (rc) return rc;
-  rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
+  rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG)
+             : gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y, nullptr, ldv, yS);
   KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
@@ -260,6 +435,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   KL(assemble_alm_launch(as, p, Y, ldv, ctx->stream), "assemble (ALM) kernel");
   // accurate cost f^ = sum R^2 + (2/sigma) <T, S + C> + ||T||^2/sigma^2 (reading R29)
   KL(alm_cost_launch(ctx->d_scal + S_ALM, sigma, cost ? cost : ctx->d_scal + S_COST, ctx->stream), "alm cost");
+  if (p > 64) return costgrad_generic(ctx, n, p, Mout, ldm, Y, ldv, G, nullptr, egrad, rgrad, rho, nullptr);
   SymvArgs a = base_symv(ctx, n, p, Mout, ldm);
   a.V = Y;
   a.ldv = ldv;
@@ -282,10 +458,12 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
             const double *G, double *K, const double *rho, double *wZ, double *hvp) {
   Problem &P = ctx->prob;
   const int n = (int)P.n;
-  int rc = gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
+  int rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, U, nullptr, K, nullptr)
+                  : gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
   KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
+  if (p > 64) return hvp_generic(ctx, n, p, M, ldm, Y, ldv, U, G, K, rho, P.amap.ptr, P.ld, wZ, hvp);
   SymvArgs a = base_symv(ctx, n, p, M, ldm);
   a.V = U;
   a.ldv = ldv;
@@ -496,6 +674,8 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->red_part.release();
   ctx->gram_part.release();
   ctx->symv_part.release();
+  ctx->big_P.release();
+  ctx->big_W.release();
   ctx->tile_cnt.release();
   ctx->tile_scal.release();
   ctx->sub_G.release();
@@ -702,7 +882,7 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   if (!ctx || !prm) return DRSDP_ERR_INVALID_ARG;
   const drsdp_params &q = *prm;
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
-        q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= 64 && q.max_outer >= 1 && q.max_rtr >= 1 &&
+        q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;
@@ -712,7 +892,8 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
 int drsdp_set_initial_factor(drsdp_ctx *ctx, int32_t p, const double *Y0) {
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "set_initial_factor before set_problem");
-  if (p < 1 || p > 64 || !Y0) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_initial_factor: 1 <= p <= 64");
+  if (p < 1 || p > DRSDP_MAX_P || !Y0)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_initial_factor: need 1 <= p <= DRSDP_MAX_P");
   const int64_t n = ctx->prob.n;
   ctx->h_Y0.assign(Y0, Y0 + (size_t)n * p);
   for (int64_t i = 0; i < n; ++i) {
@@ -752,14 +933,16 @@ int drsdp_subproblem_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->sub_M) return set_error(ctx, DRSDP_ERR_STATE, "subproblem_eval before set_subproblem_matrix");
-  if (p < 1 || p > 64 || !Y_dev || (flags & ~3) || !flags)
-    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval: need 1 <= p <= 64, flags in {1,2,3}");
+  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || (flags & ~3) || !flags)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval: need 1 <= p <= DRSDP_MAX_P, flags in {1,2,3}");
   if ((flags & DRSDP_EVAL_HVP) && (!U_dev || !hvp_dev))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval: HVP needs U and hvp");
   if ((flags & DRSDP_EVAL_HVP) && !(flags & DRSDP_EVAL_COSTGRAD) &&
       !(ctx->sub_cached_valid && ctx->sub_cached_Y == Y_dev && ctx->sub_cached_p == p))
     return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y");
   const int n = (int)ctx->sub_n;
+  CK(ctx->sub_G.ensure((size_t)2 * p * p), "alloc G");
+  CK(ctx->sub_K.ensure((size_t)p * p), "alloc K");
   int rc = eval_fixed(ctx, flags, n, p, ctx->sub_M, ctx->sub_ldm, Y_dev, p, U_dev, cost_dev, egrad_dev, rgrad_dev,
                       hvp_dev, ctx->sub_G.ptr, ctx->sub_K.ptr, ctx->sub_rho.ptr, ctx->d_scal + S_EXTRA, false);
   if (rc) return rc;
@@ -776,7 +959,7 @@ int drsdp_subproblem_eval_host(drsdp_ctx *ctx, int32_t flags, int32_t p, const d
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->sub_M) return set_error(ctx, DRSDP_ERR_STATE, "subproblem_eval_host before set_subproblem_matrix");
-  if (p < 1 || p > 64 || !Y || (flags & ~3) || !flags || ((flags & DRSDP_EVAL_HVP) && !U))
+  if (p < 1 || p > DRSDP_MAX_P || !Y || (flags & ~3) || !flags || ((flags & DRSDP_EVAL_HVP) && !U))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "subproblem_eval_host: bad arguments");
   cudaSetDevice(ctx->device);
   const size_t np = (size_t)ctx->sub_n * p;
@@ -845,7 +1028,7 @@ int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const doub
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "dual_update before set_problem");
   Problem &P = ctx->prob;
-  if (p < 1 || p > 64 || !Y_dev || !y_dev || !T_dev || ldt < P.n || !z_dev || !scalars_dev)
+  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !y_dev || !T_dev || ldt < P.n || !z_dev || !scalars_dev)
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "dual_update: bad arguments");
   const int n = (int)P.n;
   int rc = ensure_red(ctx, dual_update_blocks(n), 3);
@@ -869,14 +1052,7 @@ int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const doub
   da.counter = ctx->counters + C_DUAL;
   da.scal_out = ctx->d_scal + S_DUAL;
   KL(dual_update_launch(da, ctx->stream), "dual update kernel");
-  SymvArgs a = base_symv(ctx, n, p, T_dev, ldt);
-  a.V = Y_dev;
-  a.ldv = p;
-  a.Y = Y_dev;
-  a.ldy = p;
-  a.zout = z_dev;
-  a.scal_out = ctx->d_scal + S_ZSUM;
-  rc = run_symv(ctx, a, EPI_ROWDOT, false);
+  rc = rowdot_product(ctx, n, p, T_dev, ldt, Y_dev, p, z_dev, ctx->d_scal + S_ZSUM);
   if (rc) return rc;
   KL(vdot_launch(P.m, y_dev, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY, ctx->stream),
      "vdot");
@@ -899,7 +1075,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "alm_eval before set_problem");
   Problem &P = ctx->prob;
-  if (p < 1 || p > 64 || !Y_dev || !T_dev || ldt < P.n || !(sigma > 0) || (flags & ~3) || !flags)
+  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !T_dev || ldt < P.n || !(sigma > 0) || (flags & ~3) || !flags)
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: bad arguments");
   if ((flags & DRSDP_EVAL_HVP) && (!U_dev || !hvp_dev))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: HVP needs U and hvp");
@@ -908,6 +1084,8 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   CK(ctx->alm_yS.ensure(P.m), "alloc yS");
   CK(ctx->alm_wZ.ensure(P.m), "alloc wZ");
   CK(ctx->sub_rho.ensure(n), "alloc rho");
+  CK(ctx->sub_G.ensure((size_t)2 * p * p), "alloc G");
+  CK(ctx->sub_K.ensure((size_t)p * p), "alloc K");
   int rc;
   if (flags & DRSDP_EVAL_COSTGRAD) {
     rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->sub_G.ptr,

@@ -101,6 +101,7 @@ struct drsdp_ctx {
   drsdp::DBuf<double> red_part;  // grid_sum partials
   drsdp::DBuf<double> gram_part;
   drsdp::DBuf<double> symv_part;
+  drsdp::DBuf<double> big_P, big_W;  // generic-p (> 64) product outputs, n x ldv
   drsdp::DBuf<unsigned> tile_cnt;
   drsdp::DBuf<double> tile_scal;
   unsigned *counters = nullptr;  // C_TOTAL
@@ -146,7 +147,13 @@ namespace drsdp {
 int set_error(drsdp_ctx *ctx, int code, const std::string &msg);
 int cuda_check(drsdp_ctx *ctx, cudaError_t e, const char *what);
 int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p);
-int choose_splits(drsdp_ctx *ctx, int n, int bn);
+int choose_splits(drsdp_ctx *ctx, int krows, int ntiles);
+struct SymvArgs;
+int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind);
+int rowdot_product(drsdp_ctx *ctx, int n, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z,
+                   double *zsum);
+int apply_w_product(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const double *W, int r, double *out,
+                    int ldo);
 // fused subproblem evaluations on device pointers (pitch ldv for all n x p arrays)
 int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t ldm, const double *Y, int ldv,
                const double *U, double *cost, double *egrad, double *rgrad, double *hvp, double *G, double *K,

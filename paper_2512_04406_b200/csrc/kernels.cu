@@ -588,6 +588,108 @@ __global__ void combine_kernel(const double *a, double s0, const double *b, doub
   if (threadIdx.x == 0) out[0] = (a ? a[0] * s0 : 0.0) + (b ? b[0] * s1 : 0.0) + c;
 }
 
+// ----------------------------------------------------------------------------------------------
+// Generic-p row epilogues (p > 64, where the product kernels run column-chunked in RAW mode).
+// COSTGRAD (Eq. 4.6, Lemma 4.1): P = M Y, W = Y G:  E = 4 (W - P), rho_i = <E_i, y_i>,
+//   R = E - rho o Y;  scal_out = [sum_i <P_i, y_i>, ||R||^2];  cost = gg - 2 s1 + extra[0] + extra[1]
+// HVP (Eq. 4.7): Q = M U (+ A*(w) Y), W = U G + Y K:  EH = 4 (W - Q),
+//   H = EH - rowdot(EH, Y) o Y - rho o U;  scal_out = [<U, H>, 0]
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) rowepi_costgrad_kernel(int n, int p, const double *__restrict__ P, int ldp,
+                                                              const double *__restrict__ W, int ldw,
+                                                              const double *__restrict__ Y, int ldy, double *R,
+                                                              int ldr, double *E, int lde, double *rho_out,
+                                                              double *part, unsigned *counter, double *scal_out,
+                                                              const double *gg, const double *extra,
+                                                              double *cost_out) {
+  __shared__ double scratch[2 * 8];
+  double v[2] = {0.0, 0.0};
+  ROW_LOOP_BEGIN
+  const double *pr = P + (size_t)row * ldp, *wr = W + (size_t)row * ldw, *yr = Y + (size_t)row * ldy;
+  double py = 0.0, ey = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double e = 4.0 * (wr[c] - pr[c]);
+    py = fma(pr[c], yr[c], py);
+    ey = fma(e, yr[c], ey);
+  }
+  py = warp_sum(py);
+  const double rho = warp_sum(ey);
+  double rr = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double e = 4.0 * (wr[c] - pr[c]);
+    const double r = e - rho * yr[c];
+    rr = fma(r, r, rr);
+    if (R) R[(size_t)row * ldr + c] = r;
+    if (E) E[(size_t)row * lde + c] = e;
+  }
+  rr = warp_sum(rr);
+  if (lane == 0) {
+    if (rho_out) rho_out[row] = rho;
+    v[0] = py;
+    v[1] = rr;
+  }
+  ROW_LOOP_END
+  if (grid_sum<2>(v, part, counter, scal_out, scratch) && threadIdx.x == 0 && cost_out)
+    cost_out[0] = gg[0] - 2.0 * v[0] + extra[0] + extra[1];
+}
+
+__global__ void __launch_bounds__(256) rowepi_hvp_kernel(int n, int p, const double *__restrict__ Q, int ldq,
+                                                         const double *__restrict__ W, int ldw,
+                                                         const double *__restrict__ Y, int ldy,
+                                                         const double *__restrict__ U, int ldu,
+                                                         const double *__restrict__ rho, double *H, int ldh,
+                                                         double *part, unsigned *counter, double *scal_out) {
+  __shared__ double scratch[2 * 8];
+  double v[2] = {0.0, 0.0};
+  ROW_LOOP_BEGIN
+  const double *qr = Q + (size_t)row * ldq, *wr = W + (size_t)row * ldw;
+  const double *yr = Y + (size_t)row * ldy, *ur = U + (size_t)row * ldu;
+  double ehy = 0.0;
+  for (int c = lane; c < p; c += 32) ehy = fma(4.0 * (wr[c] - qr[c]), yr[c], ehy);
+  ehy = warp_sum(ehy);
+  const double rh = rho[row];
+  double uh = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double h = 4.0 * (wr[c] - qr[c]) - ehy * yr[c] - rh * ur[c];
+    H[(size_t)row * ldh + c] = h;
+    uh = fma(ur[c], h, uh);
+  }
+  uh = warp_sum(uh);
+  if (lane == 0) v[0] = uh;
+  ROW_LOOP_END
+  grid_sum<2>(v, part, counter, scal_out, scratch);
+}
+
+// z_i = <P_i, y_i> (P = T Y), out[0] = sum_i z_i   (Alg. 2 step 7, generic p)
+__global__ void __launch_bounds__(256) rowdot_kernel(int n, int p, const double *__restrict__ P, int ldp,
+                                                     const double *__restrict__ Y, int ldy, double *z, double *part,
+                                                     unsigned *counter, double *out) {
+  __shared__ double scratch[2 * 8];
+  double v[2] = {0.0, 0.0};
+  ROW_LOOP_BEGIN
+  double d = 0.0;
+  for (int c = lane; c < p; c += 32) d = fma(P[(size_t)row * ldp + c], Y[(size_t)row * ldy + c], d);
+  d = warp_sum(d);
+  if (lane == 0) {
+    z[row] = d;
+    v[0] = d;
+  }
+  ROW_LOOP_END
+  grid_sum<2>(v, part, counter, out, scratch);
+}
+
+// rows of X (n x r, pitch ld) scaled to unit norm in place; columns [r, ld) zeroed
+__global__ void __launch_bounds__(256) normalize_rows_kernel(int n, int r, int ld, double *X) {
+  ROW_LOOP_BEGIN
+  double *xr = X + (size_t)row * ld;
+  double s = 0.0;
+  for (int c = lane; c < r; c += 32) s = fma(xr[c], xr[c], s);
+  s = warp_sum(s);
+  const double inv = 1.0 / sqrt(s);
+  for (int c = lane; c < ld; c += 32) xr[c] = c < r ? xr[c] * inv : 0.0;
+  ROW_LOOP_END
+}
+
 // ---------------------------------------------------------------------------------------------
 static inline int rows_grid(int64_t n) { return (int)((n + 7) / 8); }
 
@@ -655,6 +757,31 @@ cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsign
 cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,
                            cudaStream_t st) {
   combine_kernel<<<1, 32, 0, st>>>(a, s0, b, s1, c, out);
+  return cudaGetLastError();
+}
+
+cudaError_t rowepi_costgrad_launch(int n, int p, const double *P, int ldp, const double *W, int ldw,
+                                   const double *Y, int ldy, double *R, int ldr, double *E, int lde, double *rho_out,
+                                   double *part, unsigned *counter, double *scal_out, const double *gg,
+                                   const double *extra, double *cost_out, cudaStream_t st) {
+  rowepi_costgrad_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, P, ldp, W, ldw, Y, ldy, R, ldr, E, lde, rho_out, part,
+                                                       counter, scal_out, gg, extra, cost_out);
+  return cudaGetLastError();
+}
+cudaError_t rowepi_hvp_launch(int n, int p, const double *Q, int ldq, const double *W, int ldw, const double *Y,
+                              int ldy, const double *U, int ldu, const double *rho, double *H, int ldh, double *part,
+                              unsigned *counter, double *scal_out, cudaStream_t st) {
+  rowepi_hvp_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, Q, ldq, W, ldw, Y, ldy, U, ldu, rho, H, ldh, part, counter,
+                                                  scal_out);
+  return cudaGetLastError();
+}
+cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
+                          unsigned *counter, double *out, cudaStream_t st) {
+  rowdot_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, P, ldp, Y, ldy, z, part, counter, out);
+  return cudaGetLastError();
+}
+cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st) {
+  normalize_rows_kernel<<<rows_grid(n), 256, 0, st>>>(n, r, ld, X);
   return cudaGetLastError();
 }
 

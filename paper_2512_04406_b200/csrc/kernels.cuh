@@ -103,6 +103,16 @@ cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsign
                         cudaStream_t st);
 cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,
                            cudaStream_t st);
+cudaError_t rowepi_costgrad_launch(int n, int p, const double *P, int ldp, const double *W, int ldw,
+                                   const double *Y, int ldy, double *R, int ldr, double *E, int lde, double *rho_out,
+                                   double *part, unsigned *counter, double *scal_out, const double *gg,
+                                   const double *extra, double *cost_out, cudaStream_t st);
+cudaError_t rowepi_hvp_launch(int n, int p, const double *Q, int ldq, const double *W, int ldw, const double *Y,
+                              int ldy, const double *U, int ldu, const double *rho, double *H, int ldh, double *part,
+                              unsigned *counter, double *scal_out, cudaStream_t st);
+cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
+                          unsigned *counter, double *out, cudaStream_t st);
+cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st);
 inline int rows_blocks(int64_t n) { return (int)((n + 7) / 8); }
 
 }  // namespace drsdp

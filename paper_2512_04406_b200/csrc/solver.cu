@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -45,12 +47,12 @@ struct Point {
 
 struct SolverState {
   int64_t n = 0, m = 0, ld = 0;
-  int ldp = 64;  // pitch of n x p vectors (p <= 64)
+  int ldp = 0;  // pitch of the n x p vectors: a multiple of 64 >= p, grown with the rank (grow_pitch)
   DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2];
   DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
-  DBuf<double> T, X, W, ystar, z, Vst, Wsmall;
+  DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
   DBuf<int> devinfo;
-  DBuf<double> work;
+  DBuf<double> work, gwork;
   cusolverDnHandle_t sol = nullptr;
   Point cur, prop;
   int p = 0;
@@ -71,61 +73,12 @@ void free_solver(drsdp_ctx *ctx) {
   }
   DBuf<double> *bs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw,
                         &s->tmp, &s->K, &s->wZ, &s->T, &s->X, &s->W, &s->ystar, &s->z, &s->Vst, &s->Wsmall,
-                        &s->work};
+                        &s->work, &s->Geig, &s->Gw, &s->gwork};
   for (auto *b : bs) b->release();
   s->devinfo.release();
   if (s->sol) cusolverDnDestroy(s->sol);
   delete s;
   ctx->solver = nullptr;
-}
-
-// cyclic Jacobi eigen-decomposition of a small symmetric matrix (host), ascending eigenvalues,
-// eigenvectors in columns of V (row-major p x p)
-static void jacobi_eig(int p, std::vector<double> A, std::vector<double> &w, std::vector<double> &V) {
-  V.assign((size_t)p * p, 0.0);
-  for (int i = 0; i < p; ++i) V[i * p + i] = 1.0;
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, tot = 0.0;
-    for (int i = 0; i < p; ++i)
-      for (int j = 0; j < p; ++j) {
-        tot += A[i * p + j] * A[i * p + j];
-        if (i != j) off += A[i * p + j] * A[i * p + j];
-      }
-    if (off <= 1e-30 * tot || off == 0.0) break;
-    for (int i = 0; i < p; ++i)
-      for (int j = i + 1; j < p; ++j) {
-        const double aij = A[i * p + j];
-        if (aij == 0.0) continue;
-        const double th = (A[j * p + j] - A[i * p + i]) / (2.0 * aij);
-        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
-        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < p; ++k) {
-          const double aki = A[k * p + i], akj = A[k * p + j];
-          A[k * p + i] = c * aki - s * akj;
-          A[k * p + j] = s * aki + c * akj;
-        }
-        for (int k = 0; k < p; ++k) {
-          const double aik = A[i * p + k], ajk = A[j * p + k];
-          A[i * p + k] = c * aik - s * ajk;
-          A[j * p + k] = s * aik + c * ajk;
-        }
-        for (int k = 0; k < p; ++k) {
-          const double vki = V[k * p + i], vkj = V[k * p + j];
-          V[k * p + i] = c * vki - s * vkj;
-          V[k * p + j] = s * vki + c * vkj;
-        }
-      }
-  }
-  std::vector<int> idx(p);
-  for (int i = 0; i < p; ++i) idx[i] = i;
-  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return A[a * p + a] < A[b * p + b]; });
-  w.resize(p);
-  std::vector<double> V2((size_t)p * p);
-  for (int k = 0; k < p; ++k) {
-    w[k] = A[idx[k] * p + idx[k]];
-    for (int i = 0; i < p; ++i) V2[i * p + k] = V[i * p + idx[k]];
-  }
-  V.swap(V2);
 }
 
 static double now_s() {
@@ -249,6 +202,7 @@ struct Run {
   }
 
   // Riemannian trust region (oracle/rtr.py rtr); s->cur holds Y on entry, the result on exit.
+  bool debug = std::getenv("DRSDP_DEBUG_RTR") != nullptr;
   int rtr(int p, double grad_tol, bool warm, int &iters_out, int &tcg_out) {
     RC(costgrad_at(s->cur, p));
     if (warm) {
@@ -293,6 +247,10 @@ struct Run {
       rhonum += reg;
       rhoden += reg;
       const double rho = rhonum / rhoden;
+      if (debug)
+        std::fprintf(stderr, "  rtr %4d f=%.17e gn=%.3e Delta=%.3e tcg=%d hit=%d num=%.3e den=%.3e rho=%.4f fp=%.17e gnp=%.3e\n",
+                     it, s->cur.f, s->cur.gn, Delta, nin, (int)hit, rhonum - reg, rhoden - reg, rho, s->prop.f,
+                     s->prop.gn);
       if (rho < 0.25)
         Delta /= 4.0;
       else if (rho > 0.75 && hit)
@@ -304,39 +262,7 @@ struct Run {
   }
 };
 
-static int alloc_solver(drsdp_ctx *ctx) {
-  if (!ctx->solver) ctx->solver = new SolverState();
-  SolverState *s = ctx->solver;
-  Problem &P = ctx->prob;
-  s->n = P.n;
-  s->m = P.m;
-  s->ld = P.ld;
-  s->ldp = 64;
-  const size_t nv = (size_t)P.n * s->ldp;
-  for (int k = 0; k < 2; ++k) {
-    CK(s->Ybuf[k].ensure(nv), "alloc");
-    CK(s->Rbuf[k].ensure(nv), "alloc");
-    CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
-    CK(s->Gbuf[k].ensure(64 * 64), "alloc");
-    CK(s->rhobuf[k].ensure(P.n), "alloc");
-    CK(s->ySbuf[k].ensure(P.m), "alloc");
-  }
-  DBuf<double> *vs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw, &s->tmp};
-  for (auto *b : vs) CK(b->ensure(nv), "alloc");
-  CK(s->K.ensure(64 * 64), "alloc");
-  CK(s->wZ.ensure(P.m), "alloc");
-  CK(s->T.ensure((size_t)P.n * P.ld), "alloc T");
-  CK(s->X.ensure((size_t)P.n * P.n), "alloc X");
-  CK(s->W.ensure(P.n), "alloc W");
-  CK(s->ystar.ensure(P.m), "alloc");
-  CK(s->z.ensure(P.n), "alloc");
-  CK(s->Vst.ensure((size_t)P.n * 64), "alloc");
-  CK(s->Wsmall.ensure(64 * 64), "alloc");
-  CK(s->devinfo.ensure(1), "alloc");
-  CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large),
-                                                     (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184}) *
-                              4 + 64),
-     "alloc red");
+static void assign_points(SolverState *s) {
   for (int k = 0; k < 2; ++k) {
     Point &pt = k == 0 ? s->cur : s->prop;
     pt.Y = s->Ybuf[k].ptr;
@@ -346,10 +272,74 @@ static int alloc_solver(drsdp_ctx *ctx) {
     pt.rho = s->rhobuf[k].ptr;
     pt.yS = s->ySbuf[k].ptr;
   }
+}
+
+// (Re)allocate every n x ldp vector and p x p buffer for pitch ldp_new (a multiple of 64).
+// With keep_cur, the current factor s->cur.Y (first p columns) survives, moved to Ybuf[0].
+static int set_pitch(drsdp_ctx *ctx, int ldp_new, bool keep_cur, int p) {
+  SolverState *s = ctx->solver;
+  const int64_t n = s->n;
+  const size_t nv = (size_t)n * ldp_new;
+  DBuf<double> keep;
+  if (keep_cur) {
+    CK(keep.ensure(nv), "alloc");
+    KL(repack_launch((int)n, p, s->ldp, s->cur.Y, p, ldp_new, keep.ptr, 0, 0, nullptr, 0, ctx->stream), "repack");
+    CK(cudaStreamSynchronize(ctx->stream), "sync");
+  }
+  DBuf<double> *vs[] = {&s->Ybuf[0], &s->Ybuf[1], &s->Rbuf[0], &s->Rbuf[1], &s->eta, &s->eta2, &s->Heta,
+                        &s->Heta2,    &s->r,       &s->r2,      &s->delta,   &s->Hdelta, &s->Uw,  &s->tmp};
+  for (auto *b : vs) b->release();
+  for (auto *b : vs)
+    if (!(keep_cur && b == &s->Ybuf[0])) CK(b->ensure(nv), "alloc factor-sized vectors");
+  if (keep_cur) std::swap(s->Ybuf[0], keep);
+  const size_t pp = (size_t)ldp_new * ldp_new;
+  for (int k = 0; k < 2; ++k) CK(s->Gbuf[k].ensure(pp), "alloc G");
+  CK(s->K.ensure(pp), "alloc K");
+  CK(s->Wsmall.ensure(pp), "alloc W");
+  CK(s->Geig.ensure(pp), "alloc");
+  CK(s->Gw.ensure(ldp_new), "alloc");
+  CK(ctx->sub_G.ensure(2 * pp), "alloc G");
+  CK(ctx->sub_K.ensure(pp), "alloc K");
+  int lw = 0;
+  if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ldp_new, s->Geig.ptr,
+                                  ldp_new, s->Gw.ptr, &lw) != CUSOLVER_STATUS_SUCCESS)
+    return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd_bufferSize (Gram)");
+  CK(s->gwork.ensure((size_t)lw + 1), "alloc");
+  s->ldp = ldp_new;
+  assign_points(s);
+  return DRSDP_OK;
+}
+
+static int alloc_solver(drsdp_ctx *ctx, int p0) {
+  if (!ctx->solver) ctx->solver = new SolverState();
+  SolverState *s = ctx->solver;
+  Problem &P = ctx->prob;
+  s->n = P.n;
+  s->m = P.m;
+  s->ld = P.ld;
   if (!s->sol) {
     if (cusolverDnCreate(&s->sol) != CUSOLVER_STATUS_SUCCESS) return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnCreate");
   }
   cusolverDnSetStream(s->sol, ctx->stream);
+  for (int k = 0; k < 2; ++k) {
+    CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
+    CK(s->rhobuf[k].ensure(P.n), "alloc");
+    CK(s->ySbuf[k].ensure(P.m), "alloc");
+  }
+  s->ldp = 0;
+  RC(set_pitch(ctx, std::max(64, ((p0 + 63) / 64) * 64), false, 0));
+  CK(s->wZ.ensure(P.m), "alloc");
+  CK(s->T.ensure((size_t)P.n * P.ld), "alloc T");
+  CK(s->X.ensure((size_t)P.n * P.n), "alloc X");
+  CK(s->W.ensure(P.n), "alloc W");
+  CK(s->ystar.ensure(P.m), "alloc");
+  CK(s->z.ensure(P.n), "alloc");
+  CK(s->devinfo.ensure(1), "alloc");
+  CK(s->Vst.ensure((size_t)P.n * std::max(1, ctx->prm.escape_max)), "alloc escape vectors");
+  CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large),
+                                                     (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184}) *
+                              4 + 64),
+     "alloc red");
   int lwork = 0;
   if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)P.n, s->X.ptr,
                                   (int)P.n, s->W.ptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
@@ -391,16 +381,16 @@ extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "solve before set_problem");
   cudaSetDevice(ctx->device);
   const double t0 = now_s();
-  RC(alloc_solver(ctx));
+  const drsdp_params &prm = ctx->prm;
+  int p = ctx->p0_given ? ctx->p0_given : prm.p0;
+  RC(alloc_solver(ctx, p));
   SolverState *s = ctx->solver;
   Problem &P = ctx->prob;
-  const drsdp_params &prm = ctx->prm;
   const int n = (int)P.n;
   RC(ensure_workspace(ctx, n, 64));
   Run run{ctx, s, prm, n};
   run.sigma = prm.sigma0;
   // Y^0
-  int p = ctx->p0_given ? ctx->p0_given : prm.p0;
   std::vector<double> Y0;
   if (ctx->p0_given)
     Y0 = ctx->h_Y0;
@@ -508,27 +498,7 @@ extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
     da.scal_out = ctx->d_scal + S_DUAL;
     KL(dual_update_launch(da, ctx->stream), "dual update");
     // z = rowdot(T Y, Y)
-    {
-      SymvArgs a;
-      a.A = s->T.ptr;
-      a.lda = P.ld;
-      a.n = n;
-      a.p = p;
-      a.V = s->cur.Y;
-      a.ldv = s->ldp;
-      a.Y = s->cur.Y;
-      a.ldy = s->ldp;
-      a.zout = s->z.ptr;
-      a.scal_out = ctx->d_scal + S_ZSUM;
-      a.part = ctx->symv_part.ptr;
-      a.tile_cnt = ctx->tile_cnt.ptr;
-      a.tile_scal = ctx->tile_scal.ptr;
-      a.glob_cnt = ctx->counters + C_SYMV;
-      const int bn = symv_bn(symv_pt(p), false);
-      const int S = choose_splits(ctx, n, bn);
-      a.rows_per_split = (((n + S - 1) / S + 63) / 64) * 64;
-      KL(symv_launch(a, EPI_ROWDOT, false, S, ctx->stream), "symv rowdot");
-    }
+    RC(rowdot_product(ctx, n, p, s->T.ptr, P.ld, s->cur.Y, s->ldp, s->z.ptr, ctx->d_scal + S_ZSUM));
     KL(vdot_launch(P.m, s->ystar.ptr, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY,
                    ctx->stream),
        "vdot");
@@ -564,30 +534,41 @@ extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
     int dv = 0;
     while (dv < prm.escape_max && dv < n && lam[dv] < thresh) ++dv;
-    // rank reduction (reading R15): compress Y to its numerical rank
+    // rank reduction (reading R15): compress Y to its numerical rank. Eigenpairs of the p x p
+    // Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so row/column-major agree).
     {
-      std::vector<double> G((size_t)p * p);
-      CK(cudaMemcpyAsync(G.data(), s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToHost, ctx->stream), "read G");
+      CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
+         "copy G");
+      const int lw = (int)s->gwork.cap - 1;
+      if (cusolverDnDsyevd(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, s->Geig.ptr, p, s->Gw.ptr,
+                           s->gwork.ptr, lw, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
+        return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd (Gram)");
+      ctx->launches++;
+      std::vector<double> w(p), V((size_t)p * p);
+      CK(cudaMemcpyAsync(w.data(), s->Gw.ptr, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
+      CK(cudaMemcpyAsync(V.data(), s->Geig.ptr, sizeof(double) * p * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
       CK(cudaStreamSynchronize(ctx->stream), "sync");
-      std::vector<double> w, V;
-      jacobi_eig(p, G, w, V);
       int r = 0;
       for (int i = 0; i < p; ++i)
         if (w[i] > prm.rank_tol * prm.rank_tol * w[p - 1]) ++r;
       r = std::max(1, r);
       if (r < p) {
+        // W_r = eigenvectors of the r largest eigenvalues (ascending order: the last r columns);
+        // column k of the column-major result is V[k p + i]
         std::vector<double> Wr((size_t)p * r);
         for (int i = 0; i < p; ++i)
-          for (int c = 0; c < r; ++c) Wr[(size_t)i * r + c] = V[(size_t)i * p + (p - r + c)];
+          for (int c = 0; c < r; ++c) Wr[(size_t)i * r + c] = V[(size_t)(p - r + c) * p + i];
         CK(cudaMemcpyAsync(s->Wsmall.ptr, Wr.data(), Wr.size() * 8, cudaMemcpyHostToDevice, ctx->stream), "copy W");
-        KL(apply_w_launch(n, p, s->ldp, s->cur.Y, s->Wsmall.ptr, r, s->ldp, s->tmp.ptr, ctx->stream), "apply W");
+        RC(apply_w_product(ctx, n, p, s->cur.Y, s->ldp, s->Wsmall.ptr, r, s->tmp.ptr, s->ldp));
         CK(cudaMemcpyAsync(s->cur.Y, s->tmp.ptr, (size_t)n * s->ldp * 8, cudaMemcpyDeviceToDevice, ctx->stream),
            "copy");
+        CK(cudaStreamSynchronize(ctx->stream), "sync");
         p = r;
       }
     }
-    if (dv > 0 && p + dv > 64) dv = 64 - p;
+    if (dv > 0 && p + dv > std::min(DRSDP_MAX_P, n)) dv = std::max(0, std::min(DRSDP_MAX_P, n) - p);
     if (dv > 0) {
+      if (p + dv > s->ldp) RC(set_pitch(ctx, ((p + dv + 63) / 64) * 64, true, p));
       // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]
       std::vector<double> Vh((size_t)n * dv);
       CK(cudaMemcpyAsync(Vh.data(), s->X.ptr, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),

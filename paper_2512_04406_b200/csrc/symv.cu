@@ -18,18 +18,23 @@
 
 namespace drsdp {
 
-template <int PT, int JB, int UNR, bool GATHER, int EPI>
+template <int PT, int JB, int UNR, int MODE2, int EPI, bool ATR>
 __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
   constexpr int NW = 8, BN = 8 * JB, CB = PT / 8;
   constexpr int TILE = BN * PT;
+  constexpr bool GATHER = MODE2 == MODE2_GATHER, PAIR = MODE2 == MODE2_PAIR;
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane & 3, q = lane >> 2;
-  const int tile = blockIdx.x, split = blockIdx.y, S = gridDim.y;
-  const int n = a.n, p = a.p;
-  const int j0 = tile * BN;
+  const int split = blockIdx.y, S = gridDim.y;
+  // column chunk z covers output columns [PT z, PT z + PT) (EPI_RAW only when gridDim.z > 1)
+  const int c0 = PT * blockIdx.z;
+  const int tile = blockIdx.x + gridDim.x * blockIdx.z;  // workspace / ticket slot
+  const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;
+  const int kext = a.k > 0 ? a.k : n;
+  const int j0 = blockIdx.x * BN;
   const int kbeg = split * a.rows_per_split;
-  const int kend = min(n, kbeg + a.rows_per_split);
+  const int kend = min(kext, kbeg + a.rows_per_split);
 
   double acc[JB][CB][2];
 #pragma unroll
@@ -44,25 +49,42 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
 #pragma unroll
   for (int cb = 0; cb < CB; ++cb) vok[cb] = (8 * cb + q) < p;
 
-  const double *__restrict__ Ab = a.A + j0 + q;
-  const double *__restrict__ Vb = a.V + q;
+  // A element (i, j): A[i lda + j], or A[j lda + i] when ATR (the product is then A^T-free: out = A V)
+  const double *__restrict__ Ab = ATR ? a.A + (size_t)(j0 + q) * a.lda : a.A + j0 + q;
+  const double *__restrict__ Vb = a.V + c0 + q;
   const int32_t *__restrict__ Mb = GATHER ? a.amap + j0 + q : nullptr;
-  const double *__restrict__ Xb = GATHER ? a.X + q : nullptr;
+  const double *__restrict__ Xb = GATHER ? a.X + c0 + q : nullptr;
+  const double *__restrict__ A2b =
+      PAIR ? (ATR ? a.A2 + (size_t)(j0 + q) * a.lda2 : a.A2 + j0 + q) : nullptr;
+  const double *__restrict__ V2b = PAIR ? a.V2 + c0 + q : nullptr;
 
   for (int i0 = kbeg + 4 * warp; i0 < kend; i0 += 4 * NW * UNR) {
+    constexpr bool TWO = MODE2 != MODE2_NONE;
     double af[UNR][JB], bf[UNR][CB];
-    double gf[GATHER ? UNR : 1][GATHER ? JB : 1], xf[GATHER ? UNR : 1][GATHER ? CB : 1];
+    double gf[TWO ? UNR : 1][TWO ? JB : 1], xf[TWO ? UNR : 1][TWO ? CB : 1];
     int32_t mf[GATHER ? UNR : 1][GATHER ? JB : 1];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const int i = i0 + u * 4 * NW + r;
       const bool ok = i < kend;
-      const double *arow = Ab + (size_t)i * a.lda;
       const double *vrow = Vb + (size_t)i * a.ldv;
 #pragma unroll
-      for (int jb = 0; jb < JB; ++jb) af[u][jb] = (ok && colok[jb]) ? __ldg(arow + 8 * jb) : 0.0;
+      for (int jb = 0; jb < JB; ++jb) {
+        const double *ap = ATR ? Ab + (size_t)(8 * jb) * a.lda + i : Ab + (size_t)i * a.lda + 8 * jb;
+        af[u][jb] = (ok && colok[jb]) ? __ldg(ap) : 0.0;
+      }
 #pragma unroll
       for (int cb = 0; cb < CB; ++cb) bf[u][cb] = (ok && vok[cb]) ? __ldg(vrow + 8 * cb) : 0.0;
+      if constexpr (PAIR) {
+        const double *v2row = V2b + (size_t)i * a.ldv2;
+#pragma unroll
+        for (int jb = 0; jb < JB; ++jb) {
+          const double *ap = ATR ? A2b + (size_t)(8 * jb) * a.lda2 + i : A2b + (size_t)i * a.lda2 + 8 * jb;
+          gf[u][jb] = (ok && colok[jb]) ? __ldg(ap) : 0.0;
+        }
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) xf[u][cb] = (ok && vok[cb]) ? __ldg(v2row + 8 * cb) : 0.0;
+      }
       if constexpr (GATHER) {
         const int32_t *mrow = Mb + (size_t)i * a.ldm;
         const double *xrow = Xb + (size_t)i * a.ldx;
@@ -85,7 +107,7 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
 #pragma unroll
         for (int cb = 0; cb < CB; ++cb) {
           dmma_884(acc[jb][cb][0], acc[jb][cb][1], af[u][jb], bf[u][cb]);
-          if constexpr (GATHER) dmma_884(acc[jb][cb][0], acc[jb][cb][1], gf[u][jb], xf[u][cb]);
+          if constexpr (TWO) dmma_884(acc[jb][cb][0], acc[jb][cb][1], gf[u][jb], xf[u][cb]);
         }
   }
 
@@ -163,7 +185,7 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
 #pragma unroll
       for (int h = 0; h < CPL; ++h) {
         const int c = lane + 32 * h;
-        if (c < p) a.out[(size_t)j * a.ldo + c] = pv[h];
+        if (c < p) a.out[(size_t)j * a.ldo + c0 + c] = pv[h];
       }
     } else if constexpr (EPI == EPI_ROWDOT) {
       double d = 0.0;
@@ -285,54 +307,76 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
 }
 
 // ----------------------------------------------------------------------------------------------
-template <int PT, int JB, int UNR, bool GATHER, int EPI>
+template <int PT, int JB, int UNR, int MODE2, int EPI, bool ATR>
 static cudaError_t launch_t(const SymvArgs &a, int S, cudaStream_t st) {
   constexpr int NW = 8, BN = 8 * JB;
   constexpr int TILE = BN * PT;
   constexpr int RED = (NW * TILE > 2 * PT * PT) ? NW * TILE : 2 * PT * PT;
   const size_t smem = (size_t)(RED + TILE + 64) * 8;
-  auto k = symv_kernel<PT, JB, UNR, GATHER, EPI>;
+  auto k = symv_kernel<PT, JB, UNR, MODE2, EPI, ATR>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.n + BN - 1) / BN, S);
+  const int nz = EPI == EPI_RAW ? (a.p + PT - 1) / PT : 1;
+  dim3 grid((a.n + BN - 1) / BN, S, nz);
   k<<<grid, 256, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-int symv_bn(int pt, bool gather) {
+int symv_bn(int pt, int mode2) {
+  const bool two = mode2 != MODE2_NONE;
   if (pt <= 8) return 64;
-  if (pt <= 16) return gather ? 32 : 64;
-  if (pt <= 32) return gather ? 16 : 32;
-  return gather ? 8 : 16;
+  if (pt <= 16) return two ? 32 : 64;
+  if (pt <= 32) return two ? 16 : 32;
+  return two ? 8 : 16;
 }
 
 int symv_pt(int p) { return p <= 8 ? 8 : p <= 16 ? 16 : p <= 32 ? 32 : 64; }
 
-#define DRSDP_EPI_CASES(PT, JB, UNR, G)                                          \
-  switch (epi) {                                                                 \
-    case EPI_RAW: return launch_t<PT, JB, UNR, G, EPI_RAW>(a, S, st);            \
-    case EPI_COSTGRAD: return launch_t<PT, JB, UNR, G, EPI_COSTGRAD>(a, S, st);  \
-    case EPI_HVP: return launch_t<PT, JB, UNR, G, EPI_HVP>(a, S, st);            \
-    default: return launch_t<PT, JB, UNR, G, EPI_ROWDOT>(a, S, st);              \
-  }
+int symv_chunks(int p, int epi) { return epi == EPI_RAW ? (p + symv_pt(p) - 1) / symv_pt(p) : 1; }
 
-cudaError_t symv_launch(const SymvArgs &a, int epi, bool gather, int S, cudaStream_t st) {
-  const int pt = symv_pt(a.p);
-  if (!gather) {
-    if (pt == 8) { DRSDP_EPI_CASES(8, 8, 2, false) }
-    if (pt == 16) { DRSDP_EPI_CASES(16, 8, 2, false) }
-    if (pt == 32) { DRSDP_EPI_CASES(32, 4, 2, false) }
-    DRSDP_EPI_CASES(64, 2, 2, false)
+template <int PT, int JB, int MODE2, bool ATR>
+static cudaError_t dispatch_epi(const SymvArgs &a, int epi, int S, cudaStream_t st) {
+  if constexpr (ATR || MODE2 == MODE2_PAIR) {
+    if (epi != EPI_RAW) return cudaErrorInvalidValue;
+    return launch_t<PT, JB, 2, MODE2, EPI_RAW, ATR>(a, S, st);
+  } else if constexpr (MODE2 == MODE2_GATHER) {
+    if (epi == EPI_RAW) return launch_t<PT, JB, 2, MODE2, EPI_RAW, false>(a, S, st);
+    if (epi == EPI_HVP) return launch_t<PT, JB, 2, MODE2, EPI_HVP, false>(a, S, st);
+    return cudaErrorInvalidValue;
   } else {
-    if (pt == 8) { DRSDP_EPI_CASES(8, 8, 2, true) }
-    if (pt == 16) { DRSDP_EPI_CASES(16, 4, 2, true) }
-    if (pt == 32) { DRSDP_EPI_CASES(32, 2, 2, true) }
-    DRSDP_EPI_CASES(64, 1, 2, true)
+    switch (epi) {
+      case EPI_RAW: return launch_t<PT, JB, 2, MODE2, EPI_RAW, false>(a, S, st);
+      case EPI_COSTGRAD: return launch_t<PT, JB, 2, MODE2, EPI_COSTGRAD, false>(a, S, st);
+      case EPI_HVP: return launch_t<PT, JB, 2, MODE2, EPI_HVP, false>(a, S, st);
+      default: return launch_t<PT, JB, 2, MODE2, EPI_ROWDOT, false>(a, S, st);
+    }
   }
+}
+
+template <int MODE2, bool ATR>
+static cudaError_t dispatch_pt(const SymvArgs &a, int epi, int S, cudaStream_t st) {
+  const int pt = symv_pt(a.p);
+  if (epi != EPI_RAW && a.p > 64) return cudaErrorInvalidValue;  // fused epilogues need whole rows
+  constexpr bool two = MODE2 != MODE2_NONE;
+  if (pt == 8) return dispatch_epi<8, 8, MODE2, ATR>(a, epi, S, st);
+  if (pt == 16) return dispatch_epi<16, two ? 4 : 8, MODE2, ATR>(a, epi, S, st);
+  if (pt == 32) return dispatch_epi<32, two ? 2 : 4, MODE2, ATR>(a, epi, S, st);
+  return dispatch_epi<64, two ? 1 : 2, MODE2, ATR>(a, epi, S, st);
+}
+
+cudaError_t symv_launch(const SymvArgs &a, int epi, int mode2, bool atr, int S, cudaStream_t st) {
+  if (atr) {
+    if (mode2 == MODE2_PAIR) return dispatch_pt<MODE2_PAIR, true>(a, epi, S, st);
+    if (mode2 == MODE2_NONE) return dispatch_pt<MODE2_NONE, true>(a, epi, S, st);
+    return cudaErrorInvalidValue;
+  }
+  if (mode2 == MODE2_PAIR) return dispatch_pt<MODE2_PAIR, false>(a, epi, S, st);
+  if (mode2 == MODE2_GATHER) return dispatch_pt<MODE2_GATHER, false>(a, epi, S, st);
+  return dispatch_pt<MODE2_NONE, false>(a, epi, S, st);
 }
 
 }  // namespace drsdp

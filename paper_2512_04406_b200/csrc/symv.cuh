@@ -6,12 +6,22 @@
 namespace drsdp {
 
 enum Epi { EPI_RAW = 0, EPI_COSTGRAD = 1, EPI_HVP = 2, EPI_ROWDOT = 3 };
+// second product accumulated into the same tile: none, the ALM gather-product sum_i w[amap_ij] X_i,
+// or a plain second pair A2^T V2 (A2 V2 when ATR)
+enum Mode2 { MODE2_NONE = 0, MODE2_GATHER = 1, MODE2_PAIR = 2 };
 
 struct SymvArgs {
-  // symmetric operand A (n x n, row pitch lda) and the right operand V (n x p, pitch ldv)
+  // out (n x p) = A^T V with A k x n (element (i, j) at A[i lda + j]; A symmetric n x n for the
+  // subproblem product M Y), or, with ATR, out = A V with A n x k (element (j, i) at A[j lda + i]).
+  // V is k x p (pitch ldv). k = 0 means k = n.
   const double *A = nullptr;
   int64_t lda = 0;
-  int n = 0, p = 0;
+  int n = 0, p = 0, k = 0;
+  // MODE2_PAIR: second operand pair, same access pattern as (A, V)
+  const double *A2 = nullptr;
+  int64_t lda2 = 0;
+  const double *V2 = nullptr;
+  int ldv2 = 0;
   const double *V = nullptr;
   int ldv = 0;
   // optional gather-product: acc += sum_i w[amap[i, j]] X[i, :]  (ALM HVP projection term)
@@ -48,8 +58,11 @@ struct SymvArgs {
   double *cost_out = nullptr;
 };
 
-int symv_pt(int p);               // padded width used by the kernels (8, 16, 32, 64)
-int symv_bn(int pt, bool gather);  // output rows per CTA
-cudaError_t symv_launch(const SymvArgs &a, int epi, bool gather, int S, cudaStream_t st);
+int symv_pt(int p);                // padded chunk width used by the kernels (8, 16, 32, 64)
+int symv_bn(int pt, int mode2);     // output rows per CTA
+int symv_chunks(int p, int epi);    // column chunks (grid z) of one launch: RAW splits p > 64
+// EPI_RAW: any p (column chunks of 64 on grid z); fused epilogues: p <= 64.  The split-K
+// workspace needs ceil(n/BN) * chunks * S * BN * PT doubles and as many zeroed tile counters.
+cudaError_t symv_launch(const SymvArgs &a, int epi, int mode2, bool atr, int S, cudaStream_t st);
 
 }  // namespace drsdp

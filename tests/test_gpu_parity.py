@@ -85,6 +85,19 @@ def test_fixed_eval_sweep_distribution(ctx, n, p):
     check_fixed(g, o, M, Y)
 
 
+@pytest.mark.parametrize("n", [37, 300, 1000])
+@pytest.mark.parametrize("p", [65, 100, 130, 200])
+def test_fixed_eval_large_p(ctx, n, p):
+    """p > 64: column-chunked product kernel + Gram / Y G products + row epilogues."""
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    g = gpu_fixed(ctx, M, Y, U)
+    o = sp.fixed_eval(M, Y, U)
+    check_fixed(g, o, M, Y)
+    g2 = gpu_fixed(ctx, M, Y, U, ld_pad=5, flags=0)
+    check_fixed(g2, o, M, Y)
+
+
 @pytest.mark.parametrize("n,p", [(333, 16), (129, 5)])
 def test_fixed_eval_padded_pitch_and_split_calls(ctx, n, p):
     """ldm > n with NaN padding (must never be read) and HVP in a separate call."""
@@ -205,7 +218,7 @@ def _state(d, seed, sigma, p):
 
 
 @pytest.mark.parametrize("d,seed,sigma,p", [(3, 0, 1.0, 2), (5, 1, 3.0, 5), (10, 2, 10.0, 11), (12, 3, 0.5, 16),
-                                            (14, 4, 2.0, 33)])
+                                            (14, 4, 2.0, 33), (14, 5, 4.0, 80), (20, 6, 0.7, 130)])
 def test_alm_eval_parity(ctx, d, seed, sigma, p):
     from paper_2512_04406_b200 import abi
 
@@ -231,7 +244,7 @@ def test_alm_eval_parity(ctx, d, seed, sigma, p):
     assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
 
 
-@pytest.mark.parametrize("d,p", [(6, 3), (12, 7)])
+@pytest.mark.parametrize("d,p", [(6, 3), (12, 7), (14, 70)])
 def test_operator_kernels(ctx, d, p):
     """(a) assembly, (d) y-update and dual update against the oracle's plain definitions."""
     Q, c, amap, cnt, b, T, Y, U = _state(d, 5, 2.0, p)
