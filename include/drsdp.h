@@ -118,6 +118,10 @@ typedef struct {
   int32_t escape_max;                  /* at most this many escape eigenvectors per iteration     */
   int32_t mode;                        /* 0 = y-eliminated ALM subproblem (default), 1 = fixed-M  */
   uint64_t seed;                       /* Y^0 draw when no initial factor is given                */
+  double rho_reg;                      /* trust-region ratio regularisation: max(1,|f|) eps rho_reg (R12) */
+  int32_t stall_rtr;                   /* stop RTR after this many iterations without a 2x gradient-norm
+                                          decrease (0 = never; reading R30)                        */
+  int32_t reserved;
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);

@@ -73,7 +73,7 @@ def tcg(prob, ctx, Y, g, Delta, prm: RTRParams):
     return eta, Heta, j, hit
 
 
-def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25):
+def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, stall=0):
     """Minimise prob over the oblique manifold from Y. Returns (Y, info dict).
 
     warm_U: optional second-order descent direction (Thm 4.5); a curvilinear
@@ -98,9 +98,17 @@ def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25):
             t *= 0.5
     Delta = prm.delta0
     gn = math.sqrt(inner(g, g))
+    best_gn, since_best = gn, 0
     for it in range(prm.max_iter):
         if gn <= grad_tol:
             break
+        # stagnation exit (reading R30): no halving of ||grad|| in `stall` iterations
+        if gn <= 0.5 * best_gn:
+            best_gn, since_best = gn, 0
+        else:
+            since_best += 1
+            if stall > 0 and since_best > stall:
+                break
         info["iters"] += 1
         eta, Heta, nin, hit = tcg(prob, ctx, Y, g, Delta, prm)
         info["tcg"] += nin

@@ -128,6 +128,7 @@ static int gram(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const do
   g.K = K;
   g.gg = gg;
   g.max_blocks = 296;
+  g.skip = ctx->skip_flag;
   KL(gram_launch(g, ctx->stream), "gram kernel");
   return DRSDP_OK;
 }
@@ -138,6 +139,7 @@ static SymvArgs base_symv(drsdp_ctx *ctx, int n, int p, const double *A, int64_t
   a.lda = lda;
   a.n = n;
   a.p = p;
+  a.skip = ctx->skip_flag;
   return a;
 }
 
@@ -267,7 +269,7 @@ static int hvp_generic(drsdp_ctx *ctx, int n, int p, const double *M, int64_t ld
   rc = small_right(ctx, n, p, U, ldv, G, Y, K, ctx->big_W.ptr, ldv);
   if (rc) return rc;
   KL(rowepi_hvp_launch(n, p, ctx->big_P.ptr, ldv, ctx->big_W.ptr, ldv, Y, ldv, U, ldv, rho, hvp, ldv,
-                       ctx->red_part.ptr, ctx->counters + C_VEC, ctx->d_scal + S_SCAL, ctx->stream),
+                       ctx->red_part.ptr, ctx->counters + C_VEC, ctx->d_scal + S_SCAL, ctx->skip_flag, ctx->stream),
      "row epilogue (hvp)");
   return DRSDP_OK;
 }
@@ -390,6 +392,8 @@ static SegArgs seg_args(drsdp_ctx *ctx, int p, const double *Y, const double *U,
   s.is_large = P.is_large.ptr;
   s.large_ids = P.large_ids.ptr;
   s.n_large = P.n_large;
+  s.huge_ids = P.huge_ids.ptr;
+  s.n_huge = P.n_huge;
   s.cA = P.has_C ? P.cA.ptr : nullptr;
   s.Y = Y;
   s.U = U;
@@ -399,6 +403,7 @@ static SegArgs seg_args(drsdp_ctx *ctx, int p, const double *Y, const double *U,
   s.part = ctx->red_part.ptr;
   s.counter = ctx->counters + C_SEG;
   s.scal_out = ctx->d_scal + S_SEGSQ;
+  s.skip = ctx->skip_flag;
   return s;
 }
 
@@ -410,7 +415,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   const int n = (int)P.n;
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
-  rc = ensure_red(ctx, std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large), (int64_t)assemble_alm_blocks(n), 1184}), 4);
+  rc = ensure_red(ctx, std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large, P.n_huge), (int64_t)assemble_alm_blocks(n), 1184}), 4);
   if (rc) return rc;
   rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG)
              : gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
@@ -523,14 +528,16 @@ static int finalize_problem(drsdp_ctx *ctx, const double *C_host) {
         P.h_seg_pos[fill[id]++] = ((uint32_t)i << 16) | (uint32_t)j;
       }
   }
+  // segment tiers for segsum: <= 32 upper positions one thread, 33..256 one warp, > 256 one block
   std::vector<uint8_t> is_large(m, 0);
-  std::vector<int32_t> large_ids;
+  std::vector<int32_t> large_ids, huge_ids;
   for (int64_t a = 0; a < m; ++a)
     if (cnt_upper[a] > 32) {
       is_large[a] = 1;
-      large_ids.push_back((int32_t)a);
+      (cnt_upper[a] > 256 ? huge_ids : large_ids).push_back((int32_t)a);
     }
   P.n_large = (int64_t)large_ids.size();
+  P.n_huge = (int64_t)huge_ids.size();
   // device copies
   P.ld = ((n + 63) / 64) * 64;
   std::vector<int32_t> amap_pad((size_t)n * P.ld, -1);
@@ -552,6 +559,10 @@ static int finalize_problem(drsdp_ctx *ctx, const double *C_host) {
   if (P.n_large)
     CK(cudaMemcpy(P.large_ids.ptr, large_ids.data(), sizeof(int32_t) * P.n_large, cudaMemcpyHostToDevice),
        "copy large_ids");
+  CK(P.huge_ids.ensure(std::max<int64_t>(P.n_huge, 1)), "alloc huge_ids");
+  if (P.n_huge)
+    CK(cudaMemcpy(P.huge_ids.ptr, huge_ids.data(), sizeof(int32_t) * P.n_huge, cudaMemcpyHostToDevice),
+       "copy huge_ids");
   P.has_C = C_host != nullptr;
   if (P.has_C) {
     std::vector<double> cpad((size_t)n * P.ld, 0.0);
@@ -671,6 +682,7 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   P.seg_pos.release();
   P.is_large.release();
   P.large_ids.release();
+  P.huge_ids.release();
   ctx->red_part.release();
   ctx->gram_part.release();
   ctx->symv_part.release();
@@ -875,6 +887,8 @@ int drsdp_default_params(drsdp_params *o) {
   o->escape_max = 3;
   o->mode = 0;
   o->seed = 0;
+  o->rho_reg = 1e3;
+  o->stall_rtr = 0;
   return DRSDP_OK;
 }
 
@@ -883,7 +897,8 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   const drsdp_params &q = *prm;
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
-        q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0))
+        q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
+        q.rho_reg >= 0 && q.stall_rtr >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;
   return DRSDP_OK;
@@ -1015,7 +1030,7 @@ int drsdp_y_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, double *y_dev
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "y_update before set_problem");
   if (p < 1 || !Y_dev || !y_dev) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "y_update: bad arguments");
   Problem &P = ctx->prob;
-  int rc = ensure_red(ctx, segsum_blocks(P.m, P.n_large), 2);
+  int rc = ensure_red(ctx, segsum_blocks(P.m, P.n_large, P.n_huge), 2);
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y_dev, nullptr, p, y_dev);
   KL(segsum_launch(s, false, ctx->stream), "segsum kernel");

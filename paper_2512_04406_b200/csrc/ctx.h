@@ -76,8 +76,8 @@ struct Problem {
   DBuf<int64_t> seg_ptr;
   DBuf<uint32_t> seg_pos;
   DBuf<uint8_t> is_large;
-  DBuf<int32_t> large_ids;
-  int64_t n_large = 0;
+  DBuf<int32_t> large_ids, huge_ids;
+  int64_t n_large = 0, n_huge = 0;
 };
 
 struct SolverState;
@@ -101,7 +101,8 @@ struct drsdp_ctx {
   drsdp::DBuf<double> red_part;  // grid_sum partials
   drsdp::DBuf<double> gram_part;
   drsdp::DBuf<double> symv_part;
-  drsdp::DBuf<double> big_P, big_W;  // generic-p (> 64) product outputs, n x ldv
+  drsdp::DBuf<double> big_P, big_W;
+  const int *skip_flag = nullptr;  // set while device-resident tCG batches are being launched  // generic-p (> 64) product outputs, n x ldv
   drsdp::DBuf<unsigned> tile_cnt;
   drsdp::DBuf<double> tile_scal;
   unsigned *counters = nullptr;  // C_TOTAL

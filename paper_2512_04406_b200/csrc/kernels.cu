@@ -20,7 +20,8 @@ namespace drsdp {
 __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *__restrict__ Y, int ldy,
                                                    const double *__restrict__ U, int ldu, int rows_per_block,
                                                    double *part, unsigned *counter, double *G, double *K,
-                                                   double *gg) {
+                                                   double *gg, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
   extern __shared__ double sh[];
   const int pp = p * p;
   const int nval = U ? 2 * pp : pp;
@@ -92,13 +93,14 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *_
 cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
   const int nval = a.U ? 2 * a.p * a.p : a.p * a.p;
   if (nval > 32 * 256) return cudaErrorInvalidValue;
-  int nb = (a.n + 255) / 256;
+  int nb = (a.n + 31) / 32;  // >= 32 rows per block: small n still spreads over many SMs
   if (nb > a.max_blocks) nb = a.max_blocks;
   if (nb < 1) nb = 1;
   int rpb = (a.n + nb - 1) / nb;
   nb = (a.n + rpb - 1) / rpb;
   const size_t smem = (size_t)2 * 32 * a.p * 8;
-  gram_kernel<<<nb, 256, smem, st>>>(a.n, a.p, a.Y, a.ldy, a.U, a.ldu, rpb, a.part, a.counter, a.G, a.K, a.gg);
+  gram_kernel<<<nb, 256, smem, st>>>(a.n, a.p, a.Y, a.ldy, a.U, a.ldu, rpb, a.part, a.counter, a.G, a.K, a.gg,
+                                     a.skip);
   return cudaGetLastError();
 }
 
@@ -127,6 +129,7 @@ DRSDP_DEV double seg_pos_value(uint32_t pk, const double *__restrict__ Y, const 
 
 template <bool ZMODE>
 __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
+  if (a.skip && *(volatile const int *)a.skip) return;
   __shared__ double scratch[64];
   double sq = 0.0;
   if ((int)blockIdx.x < a.nb_small) {
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
       a.out[s] = acc / (double)a.cnt[s];
       if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
     }
-  } else {
+  } else if ((int)blockIdx.x < a.nb_small + a.nb_large) {
     const int lane = threadIdx.x & 31;
     const int64_t li = (int64_t)(blockIdx.x - a.nb_small) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (li < a.n_large) {
@@ -154,6 +157,20 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
         if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
       }
     }
+  } else {
+    // one block per huge segment (e.g. the constant monomial: the n diagonal positions)
+    const int s = a.huge_ids[blockIdx.x - a.nb_small - a.nb_large];
+    const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
+    double acc[1] = {0.0};
+    for (int64_t k = b0 + threadIdx.x; k < b1; k += blockDim.x)
+      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+    block_sum<1>(acc, scratch);
+    if (threadIdx.x == 0) {
+      double t = acc[0];
+      if (!ZMODE && a.cA) t += a.cA[s];
+      a.out[s] = t / (double)a.cnt[s];
+      if (!ZMODE) sq = t * t / (double)a.cnt[s];
+    }
   }
   if (ZMODE) return;
   double v[1] = {sq};
@@ -163,8 +180,8 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
 cudaError_t segsum_launch(const SegArgs &a0, bool zmode, cudaStream_t st) {
   SegArgs a = a0;
   a.nb_small = (int)((a.m + 255) / 256);
-  const int nb_large = (int)((a.n_large + 7) / 8);
-  const int nb = a.nb_small + nb_large;
+  a.nb_large = (int)((a.n_large + 7) / 8);
+  const int nb = a.nb_small + a.nb_large + (int)a.n_huge;
   if (zmode)
     segsum_kernel<true><<<nb, 256, 0, st>>>(a);
   else
@@ -172,7 +189,9 @@ cudaError_t segsum_launch(const SegArgs &a0, bool zmode, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-int segsum_blocks(int64_t m, int64_t n_large) { return (int)((m + 255) / 256 + (n_large + 7) / 8); }
+int segsum_blocks(int64_t m, int64_t n_large, int64_t n_huge) {
+  return (int)((m + 255) / 256 + (n_large + 7) / 8 + n_huge);
+}
 
 // ----------------------------------------------------------------------------------------------
 // Assembly M = A*(y) - C - T/sigma (north star (a)); padding columns [n, ldm) are zeroed.
@@ -638,7 +657,9 @@ __global__ void __launch_bounds__(256) rowepi_hvp_kernel(int n, int p, const dou
                                                          const double *__restrict__ Y, int ldy,
                                                          const double *__restrict__ U, int ldu,
                                                          const double *__restrict__ rho, double *H, int ldh,
-                                                         double *part, unsigned *counter, double *scal_out) {
+                                                         double *part, unsigned *counter, double *scal_out,
+                                                         const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
   __shared__ double scratch[2 * 8];
   double v[2] = {0.0, 0.0};
   ROW_LOOP_BEGIN
@@ -687,6 +708,123 @@ __global__ void __launch_bounds__(256) normalize_rows_kernel(int n, int r, int l
   s = warp_sum(s);
   const double inv = 1.0 / sqrt(s);
   for (int c = lane; c < ld; c += 32) xr[c] = c < r ? xr[c] * inv : 0.0;
+  ROW_LOOP_END
+}
+
+// ----------------------------------------------------------------------------------------------
+// Device-resident truncated CG (Steihaug-Toint, the recurrences of oracle/rtr.py tcg).
+// ----------------------------------------------------------------------------------------------
+__global__ void tcg_init_kernel(TcgDev *st, double gnorm, double Delta, int max_iters) {
+  if (threadIdx.x) return;
+  st->r_r = gnorm * gnorm;
+  st->norm_r0 = gnorm;
+  st->e_Pe = 0.0;
+  st->e_Pd = 0.0;
+  st->d_Pd = gnorm * gnorm;
+  st->model = 0.0;
+  st->Delta2 = Delta * Delta;
+  st->alpha = 0.0;
+  st->beta = 0.0;
+  st->e_Pe_new = 0.0;
+  st->done = 0;
+  st->hit = 0;
+  st->iters = 0;
+  st->par = 0;
+  st->boundary = 0;
+  st->max_iters = max_iters;
+}
+
+__global__ void tcg_decide_kernel(TcgDev *st, const double *kappa) {
+  if (threadIdx.x || st->done) return;
+  const double dHd = *kappa;
+  st->iters += 1;
+  if (!isfinite(dHd)) {
+    st->done = 2;
+    return;
+  }
+  const double alpha = dHd != 0.0 ? st->r_r / dHd : INFINITY;
+  const double e_Pe_new = st->e_Pe + 2.0 * alpha * st->e_Pd + alpha * alpha * st->d_Pd;
+  if (dHd <= 0.0 || e_Pe_new >= st->Delta2) {
+    st->alpha = (-st->e_Pd + sqrt(st->e_Pd * st->e_Pd + st->d_Pd * (st->Delta2 - st->e_Pe))) / st->d_Pd;
+    st->boundary = 1;
+  } else {
+    st->alpha = alpha;
+    st->boundary = 0;
+    st->e_Pe_new = e_Pe_new;
+  }
+}
+
+// dots: [<eta', g>, <eta', H eta'>, <r', r'>]
+__global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, TcgDev *st, double *e0, double *e1,
+                                                         double *h0, double *h1, double *r0, double *r1,
+                                                         const double *__restrict__ d, const double *__restrict__ hd,
+                                                         const double *__restrict__ g, double *part,
+                                                         unsigned *counter) {
+  if (*(volatile const int *)&st->done) return;
+  __shared__ double scratch[3 * 8];
+  const int par = st->par, bnd = st->boundary;
+  const double a = st->alpha;
+  const double *e = par ? e1 : e0, *h = par ? h1 : h0, *r = par ? r1 : r0;
+  double *eo = par ? e0 : e1, *ho = par ? h0 : h1, *ro = par ? r0 : r1;
+  double v[3] = {0.0, 0.0, 0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  for (int c = lane; c < p; c += 32) {
+    const size_t k = o + c;
+    const double hdv = hd[k];
+    const double ev = fma(a, d[k], e[k]);
+    const double hv = fma(a, hdv, h[k]);
+    eo[k] = ev;
+    ho[k] = hv;
+    v[0] = fma(ev, g[k], v[0]);
+    v[1] = fma(ev, hv, v[1]);
+    if (!bnd) {
+      const double rv = fma(a, hdv, r[k]);
+      ro[k] = rv;
+      v[2] = fma(rv, rv, v[2]);
+    }
+  }
+  ROW_LOOP_END
+  if (!grid_sum<3>(v, part, counter, nullptr, scratch) || threadIdx.x != 0) return;
+  if (bnd) {
+    st->par = 1 - par;
+    st->hit = 1;
+    st->done = 1;
+    return;
+  }
+  const double new_model = v[0] + 0.5 * v[1];
+  if (new_model >= st->model) {  // no model decrease: keep the previous eta (oracle/rtr.py)
+    st->done = 1;
+    return;
+  }
+  st->par = 1 - par;
+  st->model = new_model;
+  st->e_Pe = st->e_Pe_new;
+  const double r_r_old = st->r_r;
+  st->r_r = v[2];
+  if (sqrt(v[2]) <= st->norm_r0 * fmin(st->norm_r0, 0.1)) {  // theta = 1, kappa = 0.1
+    st->done = 1;
+    return;
+  }
+  const double beta = v[2] / r_r_old;
+  st->e_Pd = beta * (st->e_Pd + a * st->d_Pd);
+  st->d_Pd = v[2] + beta * beta * st->d_Pd;
+  st->beta = beta;
+  if (st->iters >= st->max_iters) st->done = 1;
+}
+
+__global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, const TcgDev *st,
+                                                         const double *__restrict__ Y, const double *r0,
+                                                         const double *r1, double *d) {
+  if (*(volatile const int *)&st->done) return;
+  const double *r = st->par ? r1 : r0;
+  const double beta = st->beta;
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double s = 0.0;
+  for (int c = lane; c < p; c += 32) s = fma(fma(beta, d[o + c], -r[o + c]), Y[o + c], s);
+  s = warp_sum(s);
+  for (int c = lane; c < p; c += 32) d[o + c] = fma(beta, d[o + c], -r[o + c]) - s * Y[o + c];
   ROW_LOOP_END
 }
 
@@ -770,9 +908,9 @@ cudaError_t rowepi_costgrad_launch(int n, int p, const double *P, int ldp, const
 }
 cudaError_t rowepi_hvp_launch(int n, int p, const double *Q, int ldq, const double *W, int ldw, const double *Y,
                               int ldy, const double *U, int ldu, const double *rho, double *H, int ldh, double *part,
-                              unsigned *counter, double *scal_out, cudaStream_t st) {
+                              unsigned *counter, double *scal_out, const int *skip, cudaStream_t st) {
   rowepi_hvp_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, Q, ldq, W, ldw, Y, ldy, U, ldu, rho, H, ldh, part, counter,
-                                                  scal_out);
+                                                  scal_out, skip);
   return cudaGetLastError();
 }
 cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
@@ -782,6 +920,26 @@ cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *
 }
 cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st) {
   normalize_rows_kernel<<<rows_grid(n), 256, 0, st>>>(n, r, ld, X);
+  return cudaGetLastError();
+}
+
+cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, cudaStream_t s) {
+  tcg_init_kernel<<<1, 32, 0, s>>>(st, gnorm, Delta, max_iters);
+  return cudaGetLastError();
+}
+cudaError_t tcg_decide_launch(TcgDev *st, const double *kappa, cudaStream_t s) {
+  tcg_decide_kernel<<<1, 32, 0, s>>>(st, kappa);
+  return cudaGetLastError();
+}
+cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
+                              double *r0, double *r1, const double *d, const double *hd, const double *g,
+                              double *part, unsigned *counter, cudaStream_t s) {
+  tcg_update_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1, r0, r1, d, hd, g, part, counter);
+  return cudaGetLastError();
+}
+cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
+                              const double *r1, double *d, cudaStream_t s) {
+  tcg_newdir_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, Y, r0, r1, d);
   return cudaGetLastError();
 }
 

@@ -15,6 +15,7 @@ struct GramArgs {
   unsigned *counter = nullptr;
   double *G = nullptr, *K = nullptr, *gg = nullptr;
   int max_blocks = 296;
+  const int *skip = nullptr;  // device flag: kernel is a no-op when set
 };
 cudaError_t gram_launch(const GramArgs &a, cudaStream_t st);
 
@@ -24,8 +25,10 @@ struct SegArgs {
   const uint32_t *seg_pos = nullptr;
   const int32_t *cnt = nullptr;
   const uint8_t *is_large = nullptr;
-  const int32_t *large_ids = nullptr;
+  const int32_t *large_ids = nullptr;  // 33..256 upper positions: one warp each
   int64_t n_large = 0;
+  const int32_t *huge_ids = nullptr;   // > 256 upper positions: one block each
+  int64_t n_huge = 0;
   const double *cA = nullptr;  // A(C) or nullptr
   const double *Y = nullptr, *U = nullptr;
   int ld = 0, p = 0;
@@ -33,10 +36,11 @@ struct SegArgs {
   double *part = nullptr;
   unsigned *counter = nullptr;
   double *scal_out = nullptr;  // MODE_Y: sum_a A(S+C)_a^2 / cnt_a
-  int nb_small = 0;
+  int nb_small = 0, nb_large = 0;
+  const int *skip = nullptr;  // device flag: kernel is a no-op when set
 };
 cudaError_t segsum_launch(const SegArgs &a, bool zmode, cudaStream_t st);
-int segsum_blocks(int64_t m, int64_t n_large);
+int segsum_blocks(int64_t m, int64_t n_large, int64_t n_huge);
 
 struct AssembleArgs {
   int n = 0;
@@ -109,7 +113,31 @@ cudaError_t rowepi_costgrad_launch(int n, int p, const double *P, int ldp, const
                                    const double *extra, double *cost_out, cudaStream_t st);
 cudaError_t rowepi_hvp_launch(int n, int p, const double *Q, int ldq, const double *W, int ldw, const double *Y,
                               int ldy, const double *U, int ldu, const double *rho, double *H, int ldh, double *part,
-                              unsigned *counter, double *scal_out, cudaStream_t st);
+                              unsigned *counter, double *scal_out, const int *skip, cudaStream_t st);
+
+// ---- device-resident truncated CG (Steihaug-Toint; oracle/rtr.py tcg) ----------------------
+// The scalar recurrences live in device memory; every kernel of an iteration is a no-op once
+// `done` is set, so the host launches batches of iterations and synchronises once per batch.
+struct TcgDev {
+  double r_r, norm_r0, e_Pe, e_Pd, d_Pd, model, Delta2, alpha, beta, e_Pe_new;
+  int done;      // 0 running, 1 finished, 2 non-finite curvature
+  int hit;       // stopped on the trust-region boundary
+  int iters;     // Hessian-vector products used
+  int par;       // which of the ping-pong buffers (0/1) holds eta, H eta, r
+  int boundary;  // this iteration steps to the boundary
+  int max_iters;
+};
+cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, cudaStream_t s);
+// after H delta: kappa = <delta, H delta> (device scalar) -> alpha or the boundary step tau
+cudaError_t tcg_decide_launch(TcgDev *st, const double *kappa, cudaStream_t s);
+// eta' = eta + alpha delta, (H eta)' = H eta + alpha H delta, r' = r + alpha H delta, then the
+// model / residual decisions (last block)
+cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
+                              double *r0, double *r1, const double *d, const double *hd, const double *g,
+                              double *part, unsigned *counter, cudaStream_t s);
+// delta = P_Y(-r + beta delta) in place
+cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
+                              const double *r1, double *d, cudaStream_t s);
 cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
                           unsigned *counter, double *out, cudaStream_t st);
 cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st);

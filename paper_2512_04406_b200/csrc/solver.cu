@@ -53,6 +53,8 @@ struct SolverState {
   DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
   DBuf<int> devinfo;
   DBuf<double> work, gwork;
+  DBuf<TcgDev> tcg;              // device-resident tCG scalars
+  TcgDev *h_tcg = nullptr;       // pinned mirror
   cusolverDnHandle_t sol = nullptr;
   Point cur, prop;
   int p = 0;
@@ -76,6 +78,8 @@ void free_solver(drsdp_ctx *ctx) {
                         &s->work, &s->Geig, &s->Gw, &s->gwork};
   for (auto *b : bs) b->release();
   s->devinfo.release();
+  s->tcg.release();
+  if (s->h_tcg) cudaFreeHost(s->h_tcg);
   if (s->sol) cusolverDnDestroy(s->sol);
   delete s;
   ctx->solver = nullptr;
@@ -115,7 +119,6 @@ struct Run {
     return DRSDP_OK;
   }
   int hvp_at(Point &P, int p, const double *U, double *H) {
-    ++hvp;
     if (!fixed_mode()) return alm_hvp(ctx, p, P.M, s->ld, P.Y, s->ldp, U, P.G, s->K.ptr, P.rho, s->wZ.ptr, H);
     return eval_fixed(ctx, DRSDP_EVAL_HVP, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, U, nullptr, nullptr, nullptr, H,
                       ctx->sub_G.ptr, s->K.ptr, P.rho, nullptr, true);
@@ -131,7 +134,9 @@ struct Run {
   }
   void swap_pts() { std::swap(s->cur, s->prop); }
 
-  // Steihaug-Toint truncated CG (oracle/rtr.py tcg), device vectors, scalar decisions on host.
+  // Steihaug-Toint truncated CG (oracle/rtr.py tcg), device-resident: the scalar recurrences run
+  // in tcg_decide / tcg_update (kernels.cu); the host launches batches of iterations (every
+  // kernel is a no-op once the device flag `done` is set) and synchronises once per batch.
   int tcg(int p, double Delta, int max_tcg, int &iters, bool &hit) {
     Point &C = s->cur;
     const size_t bytes = (size_t)n * s->ldp * 8;
@@ -139,54 +144,46 @@ struct Run {
     CK(cudaMemsetAsync(s->Heta.ptr, 0, bytes, ctx->stream), "memset");
     CK(cudaMemcpyAsync(s->r.ptr, C.R, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
     CK(cudaMemsetAsync(s->delta.ptr, 0, bytes, ctx->stream), "memset");
-    double r_r = C.gn * C.gn;
-    const double norm_r0 = C.gn;
     KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, 0.0, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
                      ctx->d_scal + S_DOTS, ctx->stream),
        "newdir");
-    double e_Pe = 0.0, e_Pd = 0.0, d_Pd = r_r, model = 0.0;
+    TcgDev *st = s->tcg.ptr;
+    KL(tcg_init_launch(st, C.gn, Delta, max_tcg, ctx->stream), "tcg init");
+    int batch = 2;
     hit = false;
     iters = 0;
-    for (int j = 1; j <= max_tcg; ++j) {
-      iters = j;
-      RC(hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr));
-      RC(read_scalars(ctx, S_SCAL, 1));
-      const double d_Hd = ctx->h_scal[S_SCAL];
-      if (!std::isfinite(d_Hd)) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
-      const double alpha = d_Hd != 0.0 ? r_r / d_Hd : INFINITY;
-      const double e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd;
-      if (d_Hd <= 0 || e_Pe_new >= Delta * Delta) {
-        const double tau = (-e_Pd + std::sqrt(e_Pd * e_Pd + d_Pd * (Delta * Delta - e_Pe))) / d_Pd;
-        KL(tcg_step_launch(n, p, s->ldp, tau, s->eta.ptr, s->delta.ptr, s->eta2.ptr, s->Heta.ptr, s->Hdelta.ptr,
-                           s->Heta2.ptr, nullptr, nullptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
-                           ctx->d_scal + S_DOTS, ctx->stream),
-           "tcg_step");
-        std::swap(s->eta, s->eta2);
-        std::swap(s->Heta, s->Heta2);
-        hit = true;
-        break;
+    for (;;) {
+      ctx->skip_flag = &st->done;
+      for (int b = 0; b < batch; ++b) {
+        int rc = hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr);
+        if (rc == DRSDP_OK) rc = cuda_check(ctx, tcg_decide_launch(st, ctx->d_scal + S_SCAL, ctx->stream), "tcg decide");
+        if (rc == DRSDP_OK)
+          rc = cuda_check(ctx,
+                          tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr,
+                                            s->r.ptr, s->r2.ptr, s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr,
+                                            ctx->counters + C_VEC, ctx->stream),
+                          "tcg update");
+        if (rc == DRSDP_OK)
+          rc = cuda_check(ctx, tcg_newdir_launch(n, p, s->ldp, st, C.Y, s->r.ptr, s->r2.ptr, s->delta.ptr, ctx->stream),
+                          "tcg newdir");
+        ctx->launches += 3;
+        if (rc) {
+          ctx->skip_flag = nullptr;
+          return rc;
+        }
       }
-      KL(tcg_step_launch(n, p, s->ldp, alpha, s->eta.ptr, s->delta.ptr, s->eta2.ptr, s->Heta.ptr, s->Hdelta.ptr,
-                         s->Heta2.ptr, s->r.ptr, s->r2.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
-                         ctx->d_scal + S_DOTS, ctx->stream),
-         "tcg_step");
-      RC(read_scalars(ctx, S_DOTS, 3));
-      const double new_model = ctx->h_scal[S_DOTS] + 0.5 * ctx->h_scal[S_DOTS + 1];
-      if (new_model >= model) break;  // no model decrease: keep the previous eta
+      ctx->skip_flag = nullptr;
+      CK(cudaMemcpyAsync(s->h_tcg, st, sizeof(TcgDev), cudaMemcpyDeviceToHost, ctx->stream), "read tcg state");
+      CK(cudaStreamSynchronize(ctx->stream), "sync");
+      if (s->h_tcg->done) break;
+      batch = std::min(2 * batch, 16);
+    }
+    if (s->h_tcg->done == 2) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
+    iters = s->h_tcg->iters;
+    hit = s->h_tcg->hit != 0;
+    if (s->h_tcg->par) {
       std::swap(s->eta, s->eta2);
       std::swap(s->Heta, s->Heta2);
-      std::swap(s->r, s->r2);
-      model = new_model;
-      e_Pe = e_Pe_new;
-      const double r_r_old = r_r;
-      r_r = ctx->h_scal[S_DOTS + 2];
-      if (std::sqrt(r_r) <= norm_r0 * std::min(norm_r0, 0.1)) break;  // theta = 1, kappa = 0.1
-      const double beta = r_r / r_r_old;
-      KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, beta, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
-                       ctx->d_scal + S_DOTS, ctx->stream),
-         "newdir");
-      e_Pd = beta * (e_Pd + alpha * d_Pd);
-      d_Pd = r_r + beta * beta * d_Pd;
     }
     return DRSDP_OK;
   }
@@ -225,25 +222,47 @@ struct Run {
     const int max_tcg = prm.max_tcg > 0 ? prm.max_tcg : std::max(1, n * (p - 1));
     iters_out = 0;
     tcg_out = 0;
+    double best_gn = s->cur.gn;
+    int since_best = 0;
     for (int it = 0; it < prm.max_rtr; ++it) {
       if (s->cur.gn <= grad_tol) break;
+      // stagnation exit (reading R30): no halving of the gradient norm in stall_rtr iterations
+      if (s->cur.gn <= 0.5 * best_gn) {
+        best_gn = s->cur.gn;
+        since_best = 0;
+      } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr) {
+        break;
+      }
       ++iters_out;
       int nin = 0;
       bool hit = false;
       RC(tcg(p, Delta, max_tcg, nin, hit));
       tcg_out += nin;
-      double d3[3];
-      RC(dots(d3, s->cur.R, s->eta.ptr, s->eta.ptr, s->Heta.ptr, nullptr, nullptr, p));
-      bool bad = false;
-      RC(retract_into(s->cur.Y, s->eta.ptr, 1.0, s->prop.Y, p, bad));
-      if (bad) {
+      hvp += nin;
+      // one synchronisation per trust-region iteration: model dots, retraction flag and the
+      // cost / gradient norm at the trial point are read back together
+      KL(dot3_launch(n, p, s->ldp, s->cur.R, s->eta.ptr, s->eta.ptr, s->Heta.ptr, nullptr, nullptr, ctx->red_part.ptr,
+                     ctx->counters + C_VEC, ctx->d_scal + S_DOTS, ctx->stream),
+         "dot3");
+      CK(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream), "memset");
+      KL(retract_launch(n, p, s->ldp, s->cur.Y, s->eta.ptr, 1.0, s->prop.Y, ctx->d_flag, ctx->stream), "retract");
+      ++costgrad;
+      RC(alm_or_fixed_costgrad(s->prop, p));
+      int flag = 0;
+      CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+      RC(read_scalars(ctx, 0, S_DOTS + 3));
+      const double d3[2] = {ctx->h_scal[S_DOTS], ctx->h_scal[S_DOTS + 1]};
+      if (flag) {
         Delta /= 4.0;
         continue;
       }
-      RC(costgrad_at(s->prop, p));
+      s->prop.f = ctx->h_scal[S_COST];
+      s->prop.gn = std::sqrt(std::max(0.0, ctx->h_scal[S_SCAL + 1]));
+      if (!std::isfinite(s->prop.f) || !std::isfinite(s->prop.gn))
+        return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite cost");
       double rhonum = s->cur.f - s->prop.f;
       double rhoden = -d3[0] - 0.5 * d3[1];
-      const double reg = std::max(1.0, std::fabs(s->cur.f)) * 2.220446049250313e-16 * 1e3;
+      const double reg = std::max(1.0, std::fabs(s->cur.f)) * 2.220446049250313e-16 * prm.rho_reg;
       rhonum += reg;
       rhoden += reg;
       const double rho = rhonum / rhoden;
@@ -335,8 +354,10 @@ static int alloc_solver(drsdp_ctx *ctx, int p0) {
   CK(s->ystar.ensure(P.m), "alloc");
   CK(s->z.ensure(P.n), "alloc");
   CK(s->devinfo.ensure(1), "alloc");
+  CK(s->tcg.ensure(1), "alloc");
+  if (!s->h_tcg) CK(cudaMallocHost(&s->h_tcg, sizeof(TcgDev)), "alloc pinned");
   CK(s->Vst.ensure((size_t)P.n * std::max(1, ctx->prm.escape_max)), "alloc escape vectors");
-  CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large),
+  CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large, P.n_huge),
                                                      (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184}) *
                               4 + 64),
      "alloc red");
@@ -466,6 +487,8 @@ extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
       sg.is_large = P.is_large.ptr;
       sg.large_ids = P.large_ids.ptr;
       sg.n_large = P.n_large;
+      sg.huge_ids = P.huge_ids.ptr;
+      sg.n_huge = P.n_huge;
       sg.cA = P.has_C ? P.cA.ptr : nullptr;
       sg.Y = s->cur.Y;
       sg.ld = s->ldp;

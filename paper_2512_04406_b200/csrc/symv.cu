@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
   constexpr int NW = 8, BN = 8 * JB, CB = PT / 8;
   constexpr int TILE = BN * PT;
   constexpr bool GATHER = MODE2 == MODE2_GATHER, PAIR = MODE2 == MODE2_PAIR;
+  if (a.skip && *(volatile const int *)a.skip) return;  // device-resident tCG finished (solver.cu)
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = lane & 3, q = lane >> 2;

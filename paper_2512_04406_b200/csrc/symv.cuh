@@ -17,6 +17,7 @@ struct SymvArgs {
   const double *A = nullptr;
   int64_t lda = 0;
   int n = 0, p = 0, k = 0;
+  const int *skip = nullptr;  // device flag: when non-zero at launch time the kernel does nothing
   // MODE2_PAIR: second operand pair, same access pattern as (A, V)
   const double *A2 = nullptr;
   int64_t lda2 = 0;
