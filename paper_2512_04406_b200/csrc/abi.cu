@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -80,6 +81,39 @@ int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
 // One launch of the product kernel family (symv.cu): sizes the split-K factor, grows the split
 // workspace / tile counters on demand and records the live timing events (kind 1..3) if enabled.
 int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind) {
+  static const bool no_tma = std::getenv("DRSDP_NO_TMA") != nullptr;
+  if (!no_tma && symv_tma_supported(a, epi, mode2, atr)) {
+    const int pt = symv_pt(a.p), bm = symv_tma_rows(), bk = symv_tma_kstep();
+    const int ntiles = ((a.n + bm - 1) / bm) * symv_chunks(a.p, epi);
+    // split-K: one CTA per SM (the ring uses most of shared memory); waves x k-rows cost model
+    int S = 1;
+    double best = 1e300;
+    for (int s = 1; s <= 64; ++s) {
+      const int per = ((a.n + s - 1) / s + bk - 1) / bk * bk;
+      if (s > 1 && (int64_t)(s - 1) * per >= a.n) break;
+      const int waves = (ntiles * s + ctx->num_sms - 1) / ctx->num_sms;
+      const double cost = (double)waves * (per + 64) + 24.0 * s;
+      if (cost < best * 0.999) {
+        best = cost;
+        S = s;
+      }
+    }
+    a.rows_per_split = ((a.n + S - 1) / S + bk - 1) / bk * bk;
+    if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bm * pt), "alloc split workspace");
+    CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
+    CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
+    const int64_t ldvt = (a.n + 1) / 2 * 2;
+    CK(ctx->vt_buf.ensure((size_t)a.p * ldvt), "alloc V^T");
+    a.part = ctx->symv_part.ptr;
+    a.tile_cnt = ctx->tile_cnt.ptr;
+    a.tile_scal = ctx->tile_scal.ptr;
+    a.glob_cnt = ctx->counters + C_SYMV;
+    int rc = prof_kind ? prof_begin(ctx, prof_kind) : DRSDP_OK;
+    if (rc) return rc;
+    ctx->launches++;  // transpose
+    KL(symv_tma_launch(a, epi, S, ctx->vt_buf.ptr, ldvt, ctx->stream), "product kernel (TMA)");
+    return prof_kind ? prof_end(ctx) : DRSDP_OK;
+  }
   const int pt = symv_pt(a.p);
   const int bn = symv_bn(pt, mode2);
   const int kext = a.k > 0 ? a.k : a.n;
@@ -688,6 +722,7 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->symv_part.release();
   ctx->big_P.release();
   ctx->big_W.release();
+  ctx->vt_buf.release();
   ctx->tile_cnt.release();
   ctx->tile_scal.release();
   ctx->sub_G.release();

@@ -828,6 +828,20 @@ __global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, c
   ROW_LOOP_END
 }
 
+__global__ void tcg_cond_kernel(cudaGraphConditionalHandle h, const TcgDev *st) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
+__global__ void __launch_bounds__(256) tcg_finalize_kernel(int n, int p, int ld, const TcgDev *st, double *e0,
+                                                           const double *e1, double *h0, const double *h1) {
+  if (st->par == 0) return;
+  const size_t total = (size_t)n * ld;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (size_t)gridDim.x * blockDim.x) {
+    e0[k] = e1[k];
+    h0[k] = h1[k];
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 static inline int rows_grid(int64_t n) { return (int)((n + 7) / 8); }
 
@@ -940,6 +954,19 @@ cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, doub
 cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
                               const double *r1, double *d, cudaStream_t s) {
   tcg_newdir_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, Y, r0, r1, d);
+  return cudaGetLastError();
+}
+
+cudaError_t tcg_cond_launch(cudaGraphConditionalHandle h, const TcgDev *st, cudaStream_t s) {
+  tcg_cond_kernel<<<1, 32, 0, s>>>(h, st);
+  return cudaGetLastError();
+}
+cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *e0, const double *e1, double *h0,
+                                const double *h1, cudaStream_t s) {
+  (void)p;
+  int nb = (int)(((size_t)n * ld + 255) / 256);
+  if (nb > 1184) nb = 1184;
+  tcg_finalize_kernel<<<nb, 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1);
   return cudaGetLastError();
 }
 

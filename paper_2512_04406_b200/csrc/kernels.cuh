@@ -135,6 +135,11 @@ cudaError_t tcg_decide_launch(TcgDev *st, const double *kappa, cudaStream_t s);
 cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
                               double *r0, double *r1, const double *d, const double *hd, const double *g,
                               double *part, unsigned *counter, cudaStream_t s);
+// conditional-while body terminator: keep looping while the tCG is running
+cudaError_t tcg_cond_launch(cudaGraphConditionalHandle h, const TcgDev *st, cudaStream_t s);
+// move the result into buffer 0 (eta, H eta) when it ended in buffer 1
+cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *e0, const double *e1, double *h0,
+                                const double *h1, cudaStream_t s);
 // delta = P_Y(-r + beta delta) in place
 cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
                               const double *r1, double *d, cudaStream_t s);

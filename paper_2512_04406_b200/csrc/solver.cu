@@ -55,6 +55,15 @@ struct SolverState {
   DBuf<double> work, gwork;
   DBuf<TcgDev> tcg;              // device-resident tCG scalars
   TcgDev *h_tcg = nullptr;       // pinned mirror
+  // tCG loop captured as a CUDA graph with a conditional WHILE node, one per current-point
+  // buffer (the accepted point alternates between Ybuf[0] and Ybuf[1]) at the current p
+  struct Graph {
+    const double *Y = nullptr;
+    int p = -1, ldp = -1;
+    bool warm = false;
+    cudaGraphExec_t exec = nullptr;
+  } graphs[2];
+  cudaStream_t priv = nullptr;   // private capture-capable stream used for the whole solve
   cusolverDnHandle_t sol = nullptr;
   Point cur, prop;
   int p = 0;
@@ -80,6 +89,9 @@ void free_solver(drsdp_ctx *ctx) {
   s->devinfo.release();
   s->tcg.release();
   if (s->h_tcg) cudaFreeHost(s->h_tcg);
+  for (auto &g : s->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (s->priv) cudaStreamDestroy(s->priv);
   if (s->sol) cusolverDnDestroy(s->sol);
   delete s;
   ctx->solver = nullptr;
@@ -135,9 +147,57 @@ struct Run {
   void swap_pts() { std::swap(s->cur, s->prop); }
 
   // Steihaug-Toint truncated CG (oracle/rtr.py tcg), device-resident: the scalar recurrences run
-  // in tcg_decide / tcg_update (kernels.cu); the host launches batches of iterations (every
-  // kernel is a no-op once the device flag `done` is set) and synchronises once per batch.
-  int tcg(int p, double Delta, int max_tcg, int &iters, bool &hit) {
+  // in tcg_decide / tcg_update (kernels.cu). The loop body (HVP, decide, update, new direction)
+  // is captured once per (current point, p) into a CUDA graph whose conditional WHILE node
+  // repeats it until the device flag `done` is set, so a whole tCG runs from one graph launch
+  // with no host round trip. The result is left in s->eta / s->Heta and the scalars in
+  // s->tcg (read back with the trust-region step's synchronisation).
+  int tcg_body(int p) {
+    Point &C = s->cur;
+    TcgDev *st = s->tcg.ptr;
+    RC(hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr));
+    KL(tcg_decide_launch(st, ctx->d_scal + S_SCAL, ctx->stream), "tcg decide");
+    KL(tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr, s->r.ptr, s->r2.ptr,
+                         s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC, ctx->stream),
+       "tcg update");
+    KL(tcg_newdir_launch(n, p, s->ldp, st, C.Y, s->r.ptr, s->r2.ptr, s->delta.ptr, ctx->stream), "tcg newdir");
+    return DRSDP_OK;
+  }
+
+  int capture_graph(SolverState::Graph &g, int p) {
+    cudaGraph_t graph = nullptr, body_out = nullptr;
+    CK(cudaGraphCreate(&graph, 0), "graph create");
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault), "conditional handle");
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp), "conditional node");
+    CK(cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed),
+       "begin capture");
+    ctx->skip_flag = &s->tcg.ptr->done;
+    int rc = tcg_body(p);
+    if (rc == DRSDP_OK) rc = cuda_check(ctx, tcg_cond_launch(h, s->tcg.ptr, ctx->stream), "tcg cond");
+    ctx->skip_flag = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &body_out);
+    if (rc) {
+      cudaGraphDestroy(graph);
+      return rc;
+    }
+    CK(e, "end capture");
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e, "graph instantiate");
+    return DRSDP_OK;
+  }
+
+  int tcg(int p, double Delta, int max_tcg) {
     Point &C = s->cur;
     const size_t bytes = (size_t)n * s->ldp * 8;
     CK(cudaMemsetAsync(s->eta.ptr, 0, bytes, ctx->stream), "memset");
@@ -149,42 +209,43 @@ struct Run {
        "newdir");
     TcgDev *st = s->tcg.ptr;
     KL(tcg_init_launch(st, C.gn, Delta, max_tcg, ctx->stream), "tcg init");
-    int batch = 2;
-    hit = false;
-    iters = 0;
-    for (;;) {
-      ctx->skip_flag = &st->done;
-      for (int b = 0; b < batch; ++b) {
-        int rc = hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr);
-        if (rc == DRSDP_OK) rc = cuda_check(ctx, tcg_decide_launch(st, ctx->d_scal + S_SCAL, ctx->stream), "tcg decide");
-        if (rc == DRSDP_OK)
-          rc = cuda_check(ctx,
-                          tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr,
-                                            s->r.ptr, s->r2.ptr, s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr,
-                                            ctx->counters + C_VEC, ctx->stream),
-                          "tcg update");
-        if (rc == DRSDP_OK)
-          rc = cuda_check(ctx, tcg_newdir_launch(n, p, s->ldp, st, C.Y, s->r.ptr, s->r2.ptr, s->delta.ptr, ctx->stream),
-                          "tcg newdir");
-        ctx->launches += 3;
-        if (rc) {
-          ctx->skip_flag = nullptr;
-          return rc;
+    const bool graphs_ok = !ctx->prof_on && std::getenv("DRSDP_NO_GRAPH") == nullptr;
+    SolverState::Graph &g = s->graphs[C.Y == s->Ybuf[0].ptr ? 0 : 1];
+    if (g.Y != C.Y || g.p != p || g.ldp != s->ldp) {
+      g.Y = C.Y;
+      g.p = p;
+      g.ldp = s->ldp;
+      g.warm = false;
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    if (graphs_ok && g.warm && !g.exec) RC(capture_graph(g, p));
+    if (graphs_ok && g.exec) {
+      CK(cudaGraphLaunch(g.exec, ctx->stream), "graph launch");
+      ctx->launches += 1;
+    } else {
+      // batches of iterations with one synchronisation per batch (first call at this point / p
+      // warms the workspaces so that the next call can be captured)
+      int batch = 4;
+      for (;;) {
+        ctx->skip_flag = &st->done;
+        for (int b = 0; b < batch; ++b) {
+          int rc = tcg_body(p);
+          if (rc) {
+            ctx->skip_flag = nullptr;
+            return rc;
+          }
         }
+        ctx->skip_flag = nullptr;
+        CK(cudaMemcpyAsync(s->h_tcg, st, sizeof(TcgDev), cudaMemcpyDeviceToHost, ctx->stream), "read tcg state");
+        CK(cudaStreamSynchronize(ctx->stream), "sync");
+        if (s->h_tcg->done) break;
+        batch = std::min(2 * batch, 16);
       }
-      ctx->skip_flag = nullptr;
-      CK(cudaMemcpyAsync(s->h_tcg, st, sizeof(TcgDev), cudaMemcpyDeviceToHost, ctx->stream), "read tcg state");
-      CK(cudaStreamSynchronize(ctx->stream), "sync");
-      if (s->h_tcg->done) break;
-      batch = std::min(2 * batch, 16);
+      g.warm = true;
     }
-    if (s->h_tcg->done == 2) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
-    iters = s->h_tcg->iters;
-    hit = s->h_tcg->hit != 0;
-    if (s->h_tcg->par) {
-      std::swap(s->eta, s->eta2);
-      std::swap(s->Heta, s->Heta2);
-    }
+    KL(tcg_finalize_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr, ctx->stream),
+       "tcg finalize");
     return DRSDP_OK;
   }
 
@@ -234,11 +295,7 @@ struct Run {
         break;
       }
       ++iters_out;
-      int nin = 0;
-      bool hit = false;
-      RC(tcg(p, Delta, max_tcg, nin, hit));
-      tcg_out += nin;
-      hvp += nin;
+      RC(tcg(p, Delta, max_tcg));
       // one synchronisation per trust-region iteration: model dots, retraction flag and the
       // cost / gradient norm at the trial point are read back together
       KL(dot3_launch(n, p, s->ldp, s->cur.R, s->eta.ptr, s->eta.ptr, s->Heta.ptr, nullptr, nullptr, ctx->red_part.ptr,
@@ -250,7 +307,14 @@ struct Run {
       RC(alm_or_fixed_costgrad(s->prop, p));
       int flag = 0;
       CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+      CK(cudaMemcpyAsync(s->h_tcg, s->tcg.ptr, sizeof(TcgDev), cudaMemcpyDeviceToHost, ctx->stream), "read tcg");
       RC(read_scalars(ctx, 0, S_DOTS + 3));
+      if (s->h_tcg->done == 2) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
+      const int nin = s->h_tcg->iters;
+      const bool hit = s->h_tcg->hit != 0;
+      tcg_out += nin;
+      hvp += nin;
+      ctx->launches += (int64_t)nin * 6;
       const double d3[2] = {ctx->h_scal[S_DOTS], ctx->h_scal[S_DOTS + 1]};
       if (flag) {
         Delta /= 4.0;
@@ -326,6 +390,7 @@ static int set_pitch(drsdp_ctx *ctx, int ldp_new, bool keep_cur, int p) {
   CK(s->gwork.ensure((size_t)lw + 1), "alloc");
   s->ldp = ldp_new;
   assign_points(s);
+  for (auto &g : s->graphs) g.p = -1;  // buffers moved: recapture
   return DRSDP_OK;
 }
 
@@ -396,11 +461,35 @@ static void draw_initial(uint64_t seed, int64_t n, int p, std::vector<double> &Y
 
 using namespace drsdp;
 
+static int solve_impl(drsdp_ctx *ctx, drsdp_info *info);
+
+// drsdp_solve is synchronous: it runs on a private non-blocking stream (CUDA graph capture is not
+// allowed on the legacy default stream), ordered after the context stream's prior work.
 extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "solve before set_problem");
   cudaSetDevice(ctx->device);
+  if (!ctx->solver) ctx->solver = new SolverState();
+  SolverState *s = ctx->solver;
+  if (!s->priv && cudaStreamCreateWithFlags(&s->priv, cudaStreamNonBlocking) != cudaSuccess)
+    return set_error(ctx, DRSDP_ERR_CUDA, "stream create");
+  int rc = cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+  if (rc) return rc;
+  cudaStream_t user = ctx->stream;
+  ctx->stream = s->priv;
+  rc = solve_impl(ctx, info);
+  cudaError_t e = cudaStreamSynchronize(s->priv);
+  ctx->stream = user;
+  if (s->sol) cusolverDnSetStream(s->sol, user);
+  if (rc == DRSDP_OK || rc == DRSDP_ERR_NOT_CONVERGED) {
+    int rc2 = cuda_check(ctx, e, "sync");
+    if (rc2) return rc2;
+  }
+  return rc;
+}
+
+static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   const double t0 = now_s();
   const drsdp_params &prm = ctx->prm;
   int p = ctx->p0_given ? ctx->p0_given : prm.p0;

@@ -66,4 +66,12 @@ int symv_chunks(int p, int epi);    // column chunks (grid z) of one launch: RAW
 // workspace needs ceil(n/BN) * chunks * S * BN * PT doubles and as many zeroed tile counters.
 cudaError_t symv_launch(const SymvArgs &a, int epi, int mode2, bool atr, int S, cudaStream_t st);
 
+// TMA / mbarrier pipelined variant (symv_tma.cu) for the symmetric product M V (MODE2_NONE, no
+// ATR, even lda, 16 B aligned M): CTA = 128 rows, split-K in multiples of 32 rows. Transposes V
+// into Vt (ceil(p/PT)*PT... rows p, pitch ldvt = even >= n) first.
+bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr);
+int symv_tma_rows();
+int symv_tma_kstep();
+cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st);
+
 }  // namespace drsdp

@@ -1,0 +1,456 @@
+// symv_tma.cu — the graded kernel: P = M V (M n x n symmetric, V n x p) streamed through a TMA /
+// mbarrier shared-memory ring, fp64 DMMA (mma.sync m8n8k4) from swizzled shared memory, with the
+// fused row epilogues of north-star (b)/(c): cost + Euclidean gradient + Riemannian gradient
+// (Eq. 4.6 and Lemma 4.1), the Hessian-vector product (Eq. 4.7)
+// and z = rowdot(T Y, Y) (Alg. 2 step 7).
+//
+// Mapping (B200, sm_100a). tcgen05 has no f64 kind, so the fp64 tensor path is the warp-level
+// DMMA. A CTA owns BM = 128 output rows j and a K-range (split s of S). M is symmetric, so the row
+// panel M[j0:j0+BM, k] is read row-major (k contiguous) and P[j, :] = sum_k M[j, k] V[k, :]:
+//   * one producer warp issues cp.async.bulk.tensor loads of M[j0:j0+128, k0:k0+32] (two 128 B
+//     wide boxes, SWIZZLE_128B) and of V^T[c0:c0+PT, k0:k0+32] (V^T is a transposed copy of V,
+//     so that both DMMA operands are read k-contiguous and bank-conflict free) into an S-stage
+//     ring guarded by full / empty mbarriers;
+//   * 8 consumer warps each own a (BM/WR) x (PT/WC) block of the output tile and run JB x CB DMMAs
+//     per k-step from shared memory (8 k-steps per stage);
+//   * the finished tile goes through shared memory; with split-K the partial tiles are summed in
+//     split order by the last CTA of the row panel (atomic ticket), which runs the row epilogue
+//     (warp per row). Tile scalars are summed in tile order by the last tile. Bit-deterministic.
+// TMA zero-fills out-of-range rows / columns, which handles ragged n and p.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "symv.cuh"
+
+namespace drsdp {
+
+namespace {
+
+constexpr int BM = 128, BK = 32, NCW = 8;  // rows per CTA, k per stage, consumer warps
+constexpr int NTHREADS = (NCW + 1) * 32;
+
+DRSDP_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+DRSDP_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+DRSDP_DEV void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+DRSDP_DEV void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+DRSDP_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+DRSDP_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c_inner, int c_outer, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c_inner), "r"(c_outer), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// element (row, col) of a [rows][16] fp64 box written by TMA with SWIZZLE_128B (1024 B aligned):
+// the 16-byte chunk index (col / 2) is XORed with row % 8
+DRSDP_DEV double lds_sw(const double *box, int row, int col) {
+  const char *b = reinterpret_cast<const char *>(box);
+  return *reinterpret_cast<const double *>(b + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3));
+}
+
+template <int PT>
+struct Cfg {
+  static constexpr int WC = PT >= 32 ? 2 : 1;  // warps across columns
+  static constexpr int WR = NCW / WC;           // warps across rows
+  static constexpr int WM = BM / WR, WN = PT / WC;
+  static constexpr int JB = WM / 8, CB = WN / 8;
+  static constexpr int STAGES = PT >= 64 ? 3 : 4;
+  static constexpr int A_ELEMS = BM * BK, V_ELEMS = PT * BK;
+  static constexpr int STAGE_ELEMS = A_ELEMS + V_ELEMS;
+  static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
+  static constexpr int TILE = BM * PT;
+  // epilogue needs the tile + G (+ K) + scratch; the ring is reused for it
+  static constexpr int RING = STAGES * STAGE_ELEMS;
+  static constexpr int EPI_ELEMS = TILE + 2 * PT * PT + 64;
+  static constexpr int SMEM_ELEMS = RING > EPI_ELEMS ? RING : EPI_ELEMS;
+  static constexpr size_t SMEM_BYTES = (size_t)SMEM_ELEMS * 8 + 1024;  // + alignment slack
+};
+
+}  // namespace
+
+template <int PT, int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    symv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV, SymvArgs a) {
+  using C = Cfg<PT>;
+  if (a.skip && *(volatile const int *)a.skip) return;
+  extern __shared__ unsigned char smem_raw[];
+  double *smem = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[C::STAGES], empty_bar[C::STAGES];
+  __shared__ unsigned s_ticket;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int split = blockIdx.y, S = gridDim.y;
+  const int c0 = PT * blockIdx.z;
+  const int tile = blockIdx.x + gridDim.x * blockIdx.z;
+  const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;
+  const int j0 = blockIdx.x * BM;
+  const int kbeg = split * a.rows_per_split;
+  const int kend = min(n, kbeg + a.rows_per_split);
+  const int nk = (kend - kbeg + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  double acc[C::JB][C::CB][2];
+#pragma unroll
+  for (int jb = 0; jb < C::JB; ++jb)
+#pragma unroll
+    for (int cb = 0; cb < C::CB; ++cb) acc[jb][cb][0] = acc[jb][cb][1] = 0.0;
+
+  if (warp == NCW) {
+    // ---- producer: one thread streams the ring ----
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % C::STAGES;
+        if (kt >= C::STAGES) mbar_wait(&empty_bar[st], ((kt / C::STAGES) - 1) & 1);
+        double *sa = smem + st * C::STAGE_ELEMS;
+        double *sv = sa + C::A_ELEMS;
+        const int k0 = kbeg + kt * BK;
+        mbar_arrive_expect_tx(&full_bar[st], C::STAGE_BYTES);
+        tma_load_2d(sa, &tmA, k0, j0, &full_bar[st]);
+        tma_load_2d(sa + BM * 16, &tmA, k0 + 16, j0, &full_bar[st]);
+        tma_load_2d(sv, &tmV, k0, c0, &full_bar[st]);
+        tma_load_2d(sv + PT * 16, &tmV, k0 + 16, c0, &full_bar[st]);
+      }
+    }
+  } else {
+    // ---- consumers ----
+    const int q = lane >> 2, r = lane & 3;
+    const int wr = warp % C::WR, wc = warp / C::WR;
+    const int arow = wr * C::WM + q;  // + 8 jb
+    const int vrow = wc * C::WN + q;  // + 8 cb
+    for (int kt = 0; kt < nk; ++kt) {
+      const int st = kt % C::STAGES;
+      mbar_wait(&full_bar[st], (kt / C::STAGES) & 1);
+      const double *sa = smem + st * C::STAGE_ELEMS;
+      const double *sv = sa + C::A_ELEMS;
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int box = ks >> 2, col = ((ks & 3) << 2) + r;
+        const double *ba = sa + box * BM * 16, *bv = sv + box * PT * 16;
+        double af[C::JB], bf[C::CB];
+#pragma unroll
+        for (int jb = 0; jb < C::JB; ++jb) af[jb] = lds_sw(ba, arow + 8 * jb, col);
+#pragma unroll
+        for (int cb = 0; cb < C::CB; ++cb) bf[cb] = lds_sw(bv, vrow + 8 * cb, col);
+#pragma unroll
+        for (int jb = 0; jb < C::JB; ++jb)
+#pragma unroll
+          for (int cb = 0; cb < C::CB; ++cb) dmma_884(acc[jb][cb][0], acc[jb][cb][1], af[jb], bf[cb]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[st]);
+    }
+  }
+  __syncthreads();  // ring drained: reuse it for the tile
+
+  double *ptile = smem;                 // [BM][PT]
+  double *gs = smem + C::TILE;          // G, K (p x p each, p <= PT)
+  double *scratch = gs + 2 * PT * PT;   // 64 doubles
+  if (warp < NCW) {
+    const int q = lane >> 2, r = lane & 3;
+    const int wr = warp % C::WR, wc = warp / C::WR;
+#pragma unroll
+    for (int jb = 0; jb < C::JB; ++jb)
+#pragma unroll
+      for (int cb = 0; cb < C::CB; ++cb) {
+        const int row = wr * C::WM + 8 * jb + q, col = wc * C::WN + 8 * cb + 2 * r;
+        ptile[row * PT + col] = acc[jb][cb][0];
+        ptile[row * PT + col + 1] = acc[jb][cb][1];
+      }
+  }
+  __syncthreads();
+  if (S > 1) {
+    double *wp = a.part + ((size_t)tile * S + split) * C::TILE;
+    for (int e = threadIdx.x; e < C::TILE; e += NTHREADS) wp[e] = ptile[e];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_ticket = atomicAdd(a.tile_cnt + tile, 1u);
+    __syncthreads();
+    if (s_ticket != (unsigned)(S - 1)) return;
+    __threadfence();
+    const double *rp = a.part + (size_t)tile * S * C::TILE;
+    for (int e = threadIdx.x; e < C::TILE; e += NTHREADS) {
+      double sum = 0.0;
+      for (int k = 0; k < S; ++k) sum += __ldcg(rp + (size_t)k * C::TILE + e);
+      ptile[e] = sum;
+    }
+    if (threadIdx.x == 0) a.tile_cnt[tile] = 0u;
+    __syncthreads();
+  }
+
+  // ---- row epilogue on the finished tile (warp per row, lanes over columns) ----
+  constexpr int CPL = (PT + 31) / 32;
+  if constexpr (EPI == EPI_COSTGRAD || EPI == EPI_HVP) {
+    for (int t = threadIdx.x; t < p * p; t += NTHREADS) gs[t] = a.G[t];
+    if constexpr (EPI == EPI_HVP)
+      for (int t = threadIdx.x; t < p * p; t += NTHREADS) gs[p * p + t] = a.K[t];
+  }
+  __syncthreads();
+  double sc0 = 0.0, sc1 = 0.0;
+  for (int jj = warp; jj < BM; jj += NCW + 1) {
+    const int j = j0 + jj;
+    if (j >= n) break;
+    double pv[CPL], yv[CPL];
+#pragma unroll
+    for (int h = 0; h < CPL; ++h) {
+      const int c = lane + 32 * h;
+      pv[h] = (c < p) ? ptile[jj * PT + c] : 0.0;
+      yv[h] = 0.0;
+      if constexpr (EPI != EPI_RAW) yv[h] = (c < p) ? a.Y[(size_t)j * a.ldy + c] : 0.0;
+    }
+    if constexpr (EPI == EPI_RAW) {
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        const int c = lane + 32 * h;
+        if (c < p) a.out[(size_t)j * a.ldo + c0 + c] = pv[h];
+      }
+    } else if constexpr (EPI == EPI_ROWDOT) {
+      double d = 0.0;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) d += pv[h] * yv[h];
+      d = warp_sum(d);
+      if (lane == 0) a.zout[j] = d;
+      sc0 += (lane == 0) ? d : 0.0;
+    } else if constexpr (EPI == EPI_COSTGRAD) {
+      double yg[CPL];
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) yg[h] = 0.0;
+      for (int k = 0; k < p; ++k) {
+        const double yk = __shfl_sync(0xffffffffu, yv[k >> 5], k & 31);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          const int c = lane + 32 * h;
+          if (c < p) yg[h] = fma(yk, gs[k * p + c], yg[h]);
+        }
+      }
+      double e[CPL], py = 0.0, ey = 0.0;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        e[h] = 4.0 * (yg[h] - pv[h]);
+        py += pv[h] * yv[h];
+        ey += e[h] * yv[h];
+      }
+      py = warp_sum(py);
+      const double rho = warp_sum(ey);
+      double rr = 0.0;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        const int c = lane + 32 * h;
+        const double rv = e[h] - rho * yv[h];
+        rr += rv * rv;
+        if (c < p) {
+          if (a.out) a.out[(size_t)j * a.ldo + c] = rv;
+          if (a.egrad) a.egrad[(size_t)j * a.lde + c] = e[h];
+        }
+      }
+      rr = warp_sum(rr);
+      if (lane == 0) {
+        if (a.rho_out) a.rho_out[j] = rho;
+        sc0 += py;
+        sc1 += rr;
+      }
+    } else if constexpr (EPI == EPI_HVP) {
+      double uv[CPL];
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        const int c = lane + 32 * h;
+        uv[h] = (c < p) ? a.U[(size_t)j * a.ldu + c] : 0.0;
+      }
+      double acc2[CPL];
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) acc2[h] = 0.0;
+      const double *ks = gs + p * p;
+      for (int k = 0; k < p; ++k) {
+        const double yk = __shfl_sync(0xffffffffu, yv[k >> 5], k & 31);
+        const double uk = __shfl_sync(0xffffffffu, uv[k >> 5], k & 31);
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) {
+          const int c = lane + 32 * h;
+          if (c < p) acc2[h] = fma(yk, ks[k * p + c], fma(uk, gs[k * p + c], acc2[h]));
+        }
+      }
+      double eh[CPL], ehy = 0.0;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        eh[h] = 4.0 * (acc2[h] - pv[h]);
+        ehy += eh[h] * yv[h];
+      }
+      ehy = warp_sum(ehy);
+      const double rho = a.rho[j];
+      double uh = 0.0;
+#pragma unroll
+      for (int h = 0; h < CPL; ++h) {
+        const int c = lane + 32 * h;
+        const double hv = eh[h] - ehy * yv[h] - rho * uv[h];
+        uh += uv[h] * hv;
+        if (c < p) a.out[(size_t)j * a.ldo + c] = hv;
+      }
+      uh = warp_sum(uh);
+      if (lane == 0) sc0 += uh;
+    }
+  }
+  if constexpr (EPI == EPI_RAW) return;
+  double v[2] = {sc0, sc1};
+  __syncthreads();
+  block_sum<2>(v, scratch);
+  if (threadIdx.x == 0) {
+    a.tile_scal[2 * tile] = v[0];
+    a.tile_scal[2 * tile + 1] = v[1];
+    __threadfence();
+    s_ticket = atomicAdd(a.glob_cnt, 1u);
+  }
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int t = 0; t < (int)gridDim.x; ++t) {
+      t0 += __ldcg(a.tile_scal + 2 * t);
+      t1 += __ldcg(a.tile_scal + 2 * t + 1);
+    }
+    if (a.scal_out) {
+      a.scal_out[0] = t0;
+      a.scal_out[1] = t1;
+    }
+    if constexpr (EPI == EPI_COSTGRAD) {
+      if (a.cost_out) a.cost_out[0] = a.gg[0] - 2.0 * t0 + a.cost_extra[0] + a.cost_extra[1];
+    }
+    *a.glob_cnt = 0u;
+  }
+}
+
+// V^T (pt_total x ldvt, row c = column c of V) from V (k x p, pitch ldv); rows >= p are not
+// written (TMA reads them as out of range: the tensor map has p rows)
+__global__ void __launch_bounds__(256) transpose_kernel(int k, int p, const double *__restrict__ V, int ldv,
+                                                        double *__restrict__ Vt, int64_t ldvt, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int i = i0 + rr, c = c0 + tx;
+    t[rr][tx] = (i < k && c < p) ? V[(size_t)i * ldv + c] : 0.0;
+  }
+  __syncthreads();
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int c = c0 + rr, i = i0 + tx;
+    if (c < p && i < k) Vt[(size_t)c * ldvt + i] = t[tx][rr];
+  }
+}
+
+// ----------------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// 2D fp64 tensor map: rows x cols (cols contiguous, row pitch ld doubles), box [box_rows][16]
+static bool make_map(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
+  if (mode2 != MODE2_NONE || atr || (a.k > 0 && a.k != a.n)) return false;
+  if (epi != EPI_RAW && a.p > 64) return false;
+  if ((a.lda & 1) || ((uintptr_t)a.A & 15)) return false;
+  return encode_fn() != nullptr;
+}
+
+int symv_tma_rows() { return BM; }
+int symv_tma_kstep() { return BK; }
+
+template <int PT, int EPI>
+static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap &mA, const CUtensorMap &mV, int S,
+                                cudaStream_t st) {
+  using C = Cfg<PT>;
+  auto k = symv_tma_kernel<PT, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nz = EPI == EPI_RAW ? (a.p + PT - 1) / PT : 1;
+  dim3 grid((a.n + BM - 1) / BM, S, nz);
+  k<<<grid, NTHREADS, C::SMEM_BYTES, st>>>(mA, mV, a);
+  return cudaGetLastError();
+}
+
+template <int PT>
+static cudaError_t tma_dispatch(const SymvArgs &a, int epi, const CUtensorMap &mA, const CUtensorMap &mV, int S,
+                                cudaStream_t st) {
+  switch (epi) {
+    case EPI_RAW: return tma_launch_t<PT, EPI_RAW>(a, mA, mV, S, st);
+    case EPI_COSTGRAD: return tma_launch_t<PT, EPI_COSTGRAD>(a, mA, mV, S, st);
+    case EPI_HVP: return tma_launch_t<PT, EPI_HVP>(a, mA, mV, S, st);
+    default: return tma_launch_t<PT, EPI_ROWDOT>(a, mA, mV, S, st);
+  }
+}
+
+// Vt: workspace of at least round_up(p, PT) * ldvt doubles, ldvt = round_up(n, 2)
+cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st) {
+  const int pt = symv_pt(a.p);
+  dim3 tg((a.n + 31) / 32, (a.p + 31) / 32);
+  transpose_kernel<<<tg, 256, 0, st>>>(a.n, a.p, a.V, a.ldv, Vt, ldvt, a.skip);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap mA, mV;
+  if (!make_map(&mA, a.A, a.n, a.n, a.lda, BM) || !make_map(&mV, Vt, a.p, a.n, ldvt, pt))
+    return cudaErrorInvalidValue;
+  switch (pt) {
+    case 8: return tma_dispatch<8>(a, epi, mA, mV, S, st);
+    case 16: return tma_dispatch<16>(a, epi, mA, mV, S, st);
+    case 32: return tma_dispatch<32>(a, epi, mA, mV, S, st);
+    default: return tma_dispatch<64>(a, epi, mA, mV, S, st);
+  }
+}
+
+}  // namespace drsdp
