@@ -43,16 +43,16 @@ class Params:
         self.tau2 = 1.0
         self.tol = 1e-8
         self.eig_neg_tol = 1e-9
-        self.rank_tol = 1e-6
+        self.rank_tol = 1e-4
         self.p0 = 2
         self.max_outer = 300
         self.max_rtr = 500
-        self.escape_max = 3
+        self.escape_max = 8
         self.mode = "alm"
         self.eps_scale = 1e-2
         self.eps_floor = 1e-12
         self.rho_reg = 1e3
-        self.stall_rtr = 0
+        self.stall_rtr = 10
         for k, v in kw.items():
             if not hasattr(self, k):
                 raise TypeError(f"unknown parameter {k}")

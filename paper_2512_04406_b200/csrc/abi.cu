@@ -911,7 +911,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->tau2 = 1.0;
   o->tol = 1e-8;
   o->eig_neg_tol = 1e-9;
-  o->rank_tol = 1e-6;
+  o->rank_tol = 1e-4;
   o->eps_scale = 1e-2;
   o->eps_floor = 1e-12;
   o->time_limit_s = 0.0;
@@ -919,11 +919,11 @@ int drsdp_default_params(drsdp_params *o) {
   o->max_outer = 300;
   o->max_rtr = 500;
   o->max_tcg = 0;
-  o->escape_max = 3;
+  o->escape_max = 8;
   o->mode = 0;
   o->seed = 0;
   o->rho_reg = 1e3;
-  o->stall_rtr = 0;
+  o->stall_rtr = 10;
   return DRSDP_OK;
 }
 

@@ -491,6 +491,7 @@ extern "C" int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info) {
 
 static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   const double t0 = now_s();
+  const bool verbose = std::getenv("DRSDP_VERBOSE") != nullptr;
   const drsdp_params &prm = ctx->prm;
   int p = ctx->p0_given ? ctx->p0_given : prm.p0;
   RC(alloc_solver(ctx, p));
@@ -636,6 +637,9 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     const double eta_max = std::max(eta_p, std::max(eta_d, eta_g));
     double row[13] = {(double)(k + 1), eta_p, eta_d, eta_g, eta_max, pobj, dobj, run.sigma, (double)p,
                       (double)rtr_it, (double)tcg_it, 0.0, 0.0};
+    if (verbose)
+      std::fprintf(stderr, "[drsdp] k=%d p=%d sigma=%.3e eta_p=%.3e eta_d=%.3e eta_g=%.3e dobj=%.12f rtr=%d tcg=%d t=%.2fs\n",
+                   k + 1, p, run.sigma, eta_p, eta_d, eta_g, dobj, rtr_it, tcg_it, now_s() - t0);
     if (eta_max <= prm.tol) {
       status = DRSDP_OK;
       row[12] = now_s() - t0;

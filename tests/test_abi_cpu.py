@@ -40,9 +40,15 @@ def test_no_device_means_error_not_fallback():
 def test_default_params_match_design():
     from paper_2512_04406_b200 import abi
 
+    from oracle import admm
+
     prm = abi.Context.default_params()
-    assert prm.tol == 1e-8 and prm.sigma0 == 1.0 and prm.gamma == 2.0 and prm.p0 == 2
-    assert prm.mode == 0 and prm.escape_max == 3 and prm.eig_neg_tol == 1e-9
+    o = admm.Params()
+    # the library's defaults are the oracle's (readings R9-R16, R30)
+    for k in ("sigma0", "sigma_min", "sigma_max", "gamma", "tau1", "tau2", "tol", "eig_neg_tol", "rank_tol",
+              "eps_scale", "eps_floor", "p0", "max_outer", "max_rtr", "escape_max", "rho_reg", "stall_rtr"):
+        assert getattr(prm, k) == getattr(o, k), k
+    assert prm.mode == 0 and o.mode == "alm"
 
 
 def test_product_package_does_not_import_oracle():
