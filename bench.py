@@ -327,7 +327,15 @@ def run_gpu(args):
         roof = {"bound": "hbm", "achieved": bytes_l / t_k / 1e9, "peak": hbm, "unit": "GB/s", "peak_source": hbm_src}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = "symv_kernel (COSTGRAD + HVP epilogues)"
+    # DRAM bytes per launch from the committed ncu --set full capture of this configuration
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        if tr.get("n") == n and tr.get("p") == p:
+            roof["traffic"] = tr["dram_bytes_per_launch"]
+            roof["traffic_source"] = tr["source"]
+    except Exception:
+        pass
+    roof["kernel"] = "symv_tma_kernel (TMA ring + DMMA, COSTGRAD and HVP epilogues; timing includes the V^T staging)"
     roof["per_launch_ms"] = t_k * 1e3
     roof["algorithmic_bytes_per_launch"] = bytes_l
     roof["algorithmic_flops_per_launch"] = flops_l

@@ -110,7 +110,8 @@ typedef struct {
   double gamma, tau1, tau2;            /* Eq. 5.1 constants, gamma > 1, tau2 >= tau1 > 0        */
   double tol;                          /* stop when eta_max <= tol, default 1e-8         */
   double eig_neg_tol;                  /* escape if lambda < -eig_neg_tol (1 + |lambda_max|)     */
-  double rank_tol;                     /* rank reduction: keep singular values >= rank_tol*max   */
+  double rank_tol;                     /* rank reduction: keep singular values >= rank_tol_k*max,
+                                          rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta))) (R32) */
   double eps_scale, eps_floor;         /* inner tolerance eps_k = max(0.1 min(1,eta) eps_scale, eps_floor) on ||XY|| */
   double time_limit_s;                 /* 0 = none                                                */
   int32_t p0;                          /* initial factorization size                      */
@@ -119,8 +120,8 @@ typedef struct {
   int32_t mode;                        /* 0 = y-eliminated ALM subproblem (default), 1 = fixed-M  */
   uint64_t seed;                       /* Y^0 draw when no initial factor is given                */
   double rho_reg;                      /* trust-region ratio regularisation: max(1,|f|) eps rho_reg (R12) */
-  int32_t stall_rtr;                   /* stop RTR after this many iterations without a 2x gradient-norm
-                                          decrease (0 = never; reading R30)                        */
+  int32_t stall_rtr;                   /* stagnation: stop RTR when ||grad|| has not halved within
+                                          stall_rtr iterations (0 = never; reading R30)            */
   int32_t reserved;
 } drsdp_params;
 

@@ -102,7 +102,7 @@ def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, 
     for it in range(prm.max_iter):
         if gn <= grad_tol:
             break
-        # stagnation exit (reading R30): no halving of ||grad|| in `stall` iterations
+        # stagnation exit (reading R30): ||grad|| has not halved within `stall` iterations
         if gn <= 0.5 * best_gn:
             best_gn, since_best = gn, 0
         else:

@@ -13,6 +13,7 @@
 
 #include "ctx.h"
 #include "kernels.cuh"
+#include "gram_tile.cuh"
 #include "symv.cuh"
 
 using namespace drsdp;
@@ -442,9 +443,14 @@ static SegArgs seg_args(drsdp_ctx *ctx, int p, const double *Y, const double *U,
 }
 
 // y-eliminated subproblem at Y: y(S), M(S) (materialised into Mout), cost/gradients.
+static bool use_dense(const double *Y, const double *U, int ldv) {
+  static const bool off = std::getenv("DRSDP_NO_DENSE") != nullptr;
+  return !off && gram_tile_supported(Y, U, ldv);
+}
+
 int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y, int ldv,
                  double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost, double *egrad,
-                 double *rgrad) {
+                 double *rgrad, double *Dbuf) {
   Problem &P = ctx->prob;
   const int n = (int)P.n;
   int rc = ensure_workspace(ctx, n, p);
@@ -455,6 +461,13 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
              : gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y, nullptr, ldv, yS);
+  const bool dense = Dbuf && use_dense(Y, Y, ldv);
+  if (dense) {
+    // S = Y Y^T as dense upper tiles (tensor path), then the segmented sum gathers from it
+    KL(gram_tile_launch(n, p, Y, Y, nullptr, nullptr, ldv, Dbuf, P.ld, ctx->skip_flag, ctx->stream), "gram tiles");
+    s.D = Dbuf;
+    s.ldd = P.ld;
+  }
   KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
   AssembleArgs as;
   as.n = n;
@@ -471,7 +484,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
   as.part = ctx->red_part.ptr;
   as.counter = ctx->counters + C_ASM;
   as.scal_out = ctx->d_scal + S_ALM;
-  KL(assemble_alm_launch(as, p, Y, ldv, ctx->stream), "assemble (ALM) kernel");
+  KL(assemble_alm_launch(as, p, Y, ldv, ctx->stream, dense ? Dbuf : nullptr, P.ld), "assemble (ALM) kernel");
   // accurate cost f^ = sum R^2 + (2/sigma) <T, S + C> + ||T||^2/sigma^2 (reading R29)
   KL(alm_cost_launch(ctx->d_scal + S_ALM, sigma, cost ? cost : ctx->d_scal + S_COST, ctx->stream), "alm cost");
   if (p > 64) return costgrad_generic(ctx, n, p, Mout, ldm, Y, ldv, G, nullptr, egrad, rgrad, rho, nullptr);
@@ -494,13 +507,19 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
 }
 
 int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
-            const double *G, double *K, const double *rho, double *wZ, double *hvp) {
+            const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf) {
   Problem &P = ctx->prob;
   const int n = (int)P.n;
   int rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, U, nullptr, K, nullptr)
                   : gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
+  if (Zbuf && use_dense(Y, U, ldv)) {
+    // Z = Y U^T + U Y^T = [Y U][U Y]^T as dense upper tiles
+    KL(gram_tile_launch(n, p, Y, U, U, Y, ldv, Zbuf, P.ld, ctx->skip_flag, ctx->stream), "gram tiles (Z)");
+    s.D = Zbuf;
+    s.ldd = P.ld;
+  }
   KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
   if (p > 64) return hvp_generic(ctx, n, p, M, ldm, Y, ldv, U, G, K, rho, P.amap.ptr, P.ld, wZ, hvp);
   SymvArgs a = base_symv(ctx, n, p, M, ldm);
@@ -731,6 +750,8 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->alm_M.release();
   ctx->alm_yS.release();
   ctx->alm_wZ.release();
+  ctx->alm_D.release();
+  ctx->alm_Z.release();
   ctx->host_stage.release();
   for (auto &e : ctx->prof_events) {
     cudaEventDestroy(e.first);
@@ -1138,8 +1159,9 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   CK(ctx->sub_K.ensure((size_t)p * p), "alloc K");
   int rc;
   if (flags & DRSDP_EVAL_COSTGRAD) {
+    CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
     rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->sub_G.ptr,
-                      ctx->sub_rho.ptr, cost_dev, egrad_dev, rgrad_dev);
+                      ctx->sub_rho.ptr, cost_dev, egrad_dev, rgrad_dev, ctx->alm_D.ptr);
     if (rc) return rc;
     ctx->alm_cached_valid = true;
     ctx->alm_cached_Y = Y_dev;
@@ -1151,8 +1173,9 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
     return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y, T, sigma");
   }
   if (flags & DRSDP_EVAL_HVP) {
+    CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
     rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->sub_G.ptr, ctx->sub_K.ptr, ctx->sub_rho.ptr,
-                 ctx->alm_wZ.ptr, hvp_dev);
+                 ctx->alm_wZ.ptr, hvp_dev, ctx->alm_Z.ptr);
     if (rc) return rc;
   }
   return DRSDP_OK;

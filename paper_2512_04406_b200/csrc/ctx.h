@@ -119,7 +119,7 @@ struct drsdp_ctx {
   int sub_cached_p = 0;
   bool sub_cached_valid = false;
   // ALM eval cache (ABI drsdp_alm_eval)
-  drsdp::DBuf<double> alm_M, alm_yS, alm_wZ;
+  drsdp::DBuf<double> alm_M, alm_yS, alm_wZ, alm_D, alm_Z;
   const double *alm_cached_Y = nullptr;
   const double *alm_cached_T = nullptr;
   int alm_cached_p = 0;
@@ -160,11 +160,12 @@ int apply_w_product(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, cons
 int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t ldm, const double *Y, int ldv,
                const double *U, double *cost, double *egrad, double *rgrad, double *hvp, double *G, double *K,
                double *rho, const double *cost_extra_dev, bool have_gram);
+// Dbuf / Zbuf (n x ld, optional): dense S / Z for the tensor-core segmented sums (gram_tile.cu)
 int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y, int ldv,
                  double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost, double *egrad,
-                 double *rgrad);
+                 double *rgrad, double *Dbuf);
 int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
-            const double *G, double *K, const double *rho, double *wZ, double *hvp);
+            const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf);
 int read_scalars(drsdp_ctx *ctx, int first, int count);
 void free_solver(drsdp_ctx *ctx);
 }  // namespace drsdp

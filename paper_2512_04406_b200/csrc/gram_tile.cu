@@ -1,0 +1,200 @@
+// gram_tile.cu — dense upper-triangle Gram tiles D = A1 B1^T (+ A2 B2^T) on the fp64 DMMA path,
+// operands streamed by TMA. Used to evaluate the segmented sums of the y-eliminated subproblem
+// through a dense intermediate instead of one gathered p-length dot product per position:
+//   y(S) = A(Y Y^T + C) / cnt       -> D = Y Y^T                  (Lemma 3.1)
+//   A(Z), Z = Y U^T + U Y^T         -> D = [Y U] [U Y]^T          (Prop 4.2's projection term)
+// then segsum_dense (kernels.cu) sums D over the positions of each constraint. The dense route
+// costs 2 n^2 p tensor flops + one n^2/2 write, against ~16 n^2 p bytes of L2 gathers for the
+// per-position dot products; it is the only practical route at d = 100 / 150 with p in the hundreds.
+//
+// CTA = one 128 x 128 tile (I <= J); 8 consumer warps as 2 x 4 warp tiles of 64 x 32
+// (8 x 4 DMMA m8n8k4 per k-step), one producer warp feeding a 3-stage ring of
+// [128 x 32] boxes of both operands (SWIZZLE_128B; both operands k-contiguous, conflict free).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "gram_tile.cuh"
+
+namespace drsdp {
+
+namespace {
+constexpr int TB = 128, BK = 32, NCW = 8, STAGES = 3;
+constexpr int NT = (NCW + 1) * 32;
+constexpr int WR = 2, WC = 4, WM = TB / WR, WN = TB / WC, JB = WM / 8, CB = WN / 8;
+constexpr int OP_ELEMS = TB * BK;                // one operand per stage
+constexpr int STAGE_ELEMS = 2 * OP_ELEMS;
+constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * 8 + 1024;
+
+DRSDP_DEV uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+DRSDP_DEV void bar_init(uint64_t *b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+DRSDP_DEV void bar_expect(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+DRSDP_DEV void bar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+DRSDP_DEV void bar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+DRSDP_DEV void tma2d(void *dst, const CUtensorMap *m, int ci, int co, uint64_t *b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          su32(dst)),
+      "l"(m), "r"(ci), "r"(co), "r"(su32(b))
+      : "memory");
+}
+DRSDP_DEV double ldsw(const double *box, int row, int col) {
+  const char *b = reinterpret_cast<const char *>(box);
+  return *reinterpret_cast<const double *>(b + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(NT, 1)
+    gram_tile_kernel(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
+                     const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mB2, int n, int p,
+                     int pair, double *__restrict__ D, int64_t ldd, const int *skip) {
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (I > J) return;  // upper-triangle tiles only (D symmetric; consumers read i <= j)
+  if (skip && *(volatile const int *)skip) return;
+  extern __shared__ unsigned char smem_raw[];
+  double *smem = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nk1 = (p + BK - 1) / BK;
+  const int nk = pair ? 2 * nk1 : nk1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCW) {
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % STAGES;
+        if (kt >= STAGES) bar_wait(&empty[st], ((kt / STAGES) - 1) & 1);
+        double *sa = smem + st * STAGE_ELEMS, *sb = sa + OP_ELEMS;
+        const bool second = kt >= nk1;
+        const int k0 = (second ? kt - nk1 : kt) * BK;
+        const CUtensorMap *ma = second ? &mA2 : &mA1, *mb = second ? &mB2 : &mB1;
+        bar_expect(&full[st], STAGE_BYTES);
+        tma2d(sa, ma, k0, I * TB, &full[st]);
+        tma2d(sa + TB * 16, ma, k0 + 16, I * TB, &full[st]);
+        tma2d(sb, mb, k0, J * TB, &full[st]);
+        tma2d(sb + TB * 16, mb, k0 + 16, J * TB, &full[st]);
+      }
+    }
+    return;
+  }
+  const int q = lane >> 2, r = lane & 3;
+  const int wr = warp % WR, wc = warp / WR;
+  double acc[JB][CB][2];
+#pragma unroll
+  for (int jb = 0; jb < JB; ++jb)
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) acc[jb][cb][0] = acc[jb][cb][1] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int st = kt % STAGES;
+    bar_wait(&full[st], (kt / STAGES) & 1);
+    const double *sa = smem + st * STAGE_ELEMS, *sb = sa + OP_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int box = ks >> 2, col = ((ks & 3) << 2) + r;
+      const double *ba = sa + box * TB * 16, *bb = sb + box * TB * 16;
+      double af[JB], bf[CB];
+#pragma unroll
+      for (int jb = 0; jb < JB; ++jb) af[jb] = ldsw(ba, wr * WM + 8 * jb + q, col);
+#pragma unroll
+      for (int cb = 0; cb < CB; ++cb) bf[cb] = ldsw(bb, wc * WN + 8 * cb + q, col);
+#pragma unroll
+      for (int jb = 0; jb < JB; ++jb)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) dmma_884(acc[jb][cb][0], acc[jb][cb][1], af[jb], bf[cb]);
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int jb = 0; jb < JB; ++jb) {
+    const int i = I * TB + wr * WM + 8 * jb + q;
+    if (i >= n) continue;
+#pragma unroll
+    for (int cb = 0; cb < CB; ++cb) {
+      const int j = J * TB + wc * WN + 8 * cb + 2 * r;
+      if (j + 1 < n) {
+        *reinterpret_cast<double2 *>(D + (size_t)i * ldd + j) = make_double2(acc[jb][cb][0], acc[jb][cb][1]);
+      } else if (j < n) {
+        D[(size_t)i * ldd + j] = acc[jb][cb][0];
+      }
+    }
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(f);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+static bool map_rows(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeFn fn = encoder();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)TB};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool gram_tile_supported(const double *A, const double *B, int ld) {
+  return !(ld & 1) && !((uintptr_t)A & 15) && !((uintptr_t)B & 15) && encoder() != nullptr;
+}
+
+cudaError_t gram_tile_launch(int n, int p, const double *A1, const double *B1, const double *A2, const double *B2,
+                             int ld, double *D, int64_t ldd, const int *skip, cudaStream_t st) {
+  CUtensorMap m[4];
+  if (!map_rows(&m[0], A1, n, p, ld) || !map_rows(&m[1], B1, n, p, ld)) return cudaErrorInvalidValue;
+  const bool pair = A2 != nullptr;
+  if (pair) {
+    if (!map_rows(&m[2], A2, n, p, ld) || !map_rows(&m[3], B2, n, p, ld)) return cudaErrorInvalidValue;
+  } else {
+    m[2] = m[0];
+    m[3] = m[1];
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nb = (n + TB - 1) / TB;
+  gram_tile_kernel<<<dim3(nb, nb), NT, SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], n, p, pair ? 1 : 0, D, ldd, skip);
+  return cudaGetLastError();
+}
+
+}  // namespace drsdp

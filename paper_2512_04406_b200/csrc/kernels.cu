@@ -114,8 +114,12 @@ cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
 // ----------------------------------------------------------------------------------------------
 template <bool ZMODE>
 DRSDP_DEV double seg_pos_value(uint32_t pk, const double *__restrict__ Y, const double *__restrict__ U, int ld,
-                               int p) {
+                               int p, const double *__restrict__ D, int64_t ldd) {
   const int i = pk >> 16, j = pk & 0xffff;
+  if (D) {
+    const double v = __ldg(D + (size_t)i * ldd + j);
+    return (i == j) ? v : 2.0 * v;
+  }
   const double *yi = Y + (size_t)i * ld, *yj = Y + (size_t)j * ld;
   double s = 0.0;
   if (!ZMODE) {
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     if (s < a.m && !a.is_large[s]) {
       const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
       double acc = 0.0;
-      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
       if (!ZMODE && a.cA) acc += a.cA[s];
       a.out[s] = acc / (double)a.cnt[s];
       if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
       const int s = a.large_ids[li];
       const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
       double acc = 0.0;
-      for (int64_t k = b0 + lane; k < b1; k += 32) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+      for (int64_t k = b0 + lane; k < b1; k += 32) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (!ZMODE && a.cA) acc += a.cA[s];
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
     double acc[1] = {0.0};
     for (int64_t k = b0 + threadIdx.x; k < b1; k += blockDim.x)
-      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p);
+      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
     block_sum<1>(acc, scratch);
     if (threadIdx.x == 0) {
       double t = acc[0];
@@ -240,7 +244,8 @@ __global__ void __launch_bounds__(256) assemble_alm_kernel(int n, int p, const d
                                                            const double *__restrict__ y, const double *__restrict__ C,
                                                            int64_t ldc, const double *__restrict__ T, int64_t ldt,
                                                            double inv_sigma, double *__restrict__ M, int64_t ldm,
-                                                           double *part, unsigned *counter, double *scal_out) {
+                                                           double *part, unsigned *counter, double *scal_out,
+                                                           const double *__restrict__ D, int64_t ldd) {
   __shared__ double yi_s[32][33], yj_s[32][33];
   __shared__ double mt[32][33];
   __shared__ double scratch[3 * 8];
@@ -250,7 +255,14 @@ __global__ void __launch_bounds__(256) assemble_alm_kernel(int n, int p, const d
     const int i0 = I * 32, j0 = J * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int c0 = 0; c0 < p; c0 += 32) {
+    if (D) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = i0 + ty + 8 * k, j = j0 + tx;
+        s[k] = (i < n && j < n) ? D[(size_t)i * ldd + j] : 0.0;
+      }
+    }
+    for (int c0 = 0; !D && c0 < p; c0 += 32) {
       const int cn = min(32, p - c0);
       __syncthreads();
       for (int t = threadIdx.x; t < 32 * 32; t += 256) {
@@ -301,10 +313,11 @@ __global__ void __launch_bounds__(256) assemble_alm_kernel(int n, int p, const d
   grid_sum<3>(v, part, counter, scal_out, scratch);
 }
 
-cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st) {
+cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st,
+                                const double *D, int64_t ldd) {
   dim3 grid((a.n + 31) / 32, (a.n + 31) / 32);
   assemble_alm_kernel<<<grid, 256, 0, st>>>(a.n, p, Y, ldy, a.amap, a.ldmap, a.y, a.C, a.ldc, a.T, a.ldt,
-                                            1.0 / a.sigma, a.M, a.ldm, a.part, a.counter, a.scal_out);
+                                            1.0 / a.sigma, a.M, a.ldm, a.part, a.counter, a.scal_out, D, ldd);
   if (a.ldm > a.n) {
     cudaError_t e = cudaMemset2DAsync(a.M + a.n, a.ldm * sizeof(double), 0, (a.ldm - a.n) * sizeof(double), a.n, st);
     if (e != cudaSuccess) return e;

@@ -38,6 +38,10 @@ struct SegArgs {
   double *scal_out = nullptr;  // MODE_Y: sum_a A(S+C)_a^2 / cnt_a
   int nb_small = 0, nb_large = 0;
   const int *skip = nullptr;  // device flag: kernel is a no-op when set
+  // dense mode (gram_tile.cu): the position value is D[i][j] (upper triangle, pitch ldd) instead
+  // of the p-length dot products; D = Y Y^T (MODE_Y) or Y U^T + U Y^T (MODE_Z)
+  const double *D = nullptr;
+  int64_t ldd = 0;
 };
 cudaError_t segsum_launch(const SegArgs &a, bool zmode, cudaStream_t st);
 int segsum_blocks(int64_t m, int64_t n_large, int64_t n_huge);
@@ -60,7 +64,9 @@ struct AssembleArgs {
 };
 cudaError_t assemble_launch(const AssembleArgs &a, cudaStream_t st);
 // tiled ALM assembly: M(S) plus [sum R^2, <T, S + C>, ||T||^2] in scal_out (3 doubles)
-cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st);
+// D (optional): dense S = Y Y^T upper triangle (pitch ldd) read instead of recomputing S tiles
+cudaError_t assemble_alm_launch(const AssembleArgs &a, int p, const double *Y, int ldy, cudaStream_t st,
+                                const double *D = nullptr, int64_t ldd = 0);
 cudaError_t alm_cost_launch(const double *s, double sigma, double *cost, cudaStream_t st);
 inline int assemble_alm_blocks(int n) { return ((n + 31) / 32) * ((n + 31) / 32); }
 

@@ -42,13 +42,14 @@ namespace drsdp {
 
 struct Point {
   double *Y = nullptr, *R = nullptr, *M = nullptr, *G = nullptr, *rho = nullptr, *yS = nullptr;
+  double *D = nullptr;  // dense S = Y Y^T (upper tiles) for the tensor-core segmented sums
   double f = 0.0, gn = 0.0;
 };
 
 struct SolverState {
   int64_t n = 0, m = 0, ld = 0;
   int ldp = 0;  // pitch of the n x p vectors: a multiple of 64 >= p, grown with the rank (grow_pitch)
-  DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2];
+  DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2], Dbuf[2], Zbuf;
   DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
   DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
   DBuf<int> devinfo;
@@ -81,7 +82,9 @@ void free_solver(drsdp_ctx *ctx) {
     s->Gbuf[k].release();
     s->rhobuf[k].release();
     s->ySbuf[k].release();
+    s->Dbuf[k].release();
   }
+  s->Zbuf.release();
   DBuf<double> *bs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw,
                         &s->tmp, &s->K, &s->wZ, &s->T, &s->X, &s->W, &s->ystar, &s->z, &s->Vst, &s->Wsmall,
                         &s->work, &s->Geig, &s->Gw, &s->gwork};
@@ -124,14 +127,14 @@ struct Run {
   int alm_or_fixed_costgrad(Point &P, int p) {
     if (!fixed_mode())
       return alm_costgrad(ctx, p, s->T.ptr, s->ld, sigma, P.Y, s->ldp, P.M, s->ld, P.yS, P.G, P.rho,
-                          ctx->d_scal + S_COST, nullptr, P.R);
+                          ctx->d_scal + S_COST, nullptr, P.R, P.D);
     // fixed M lives in s->Mbuf[0] (never swapped in this mode); yS = y(S) for the outer update
     RC(eval_fixed(ctx, DRSDP_EVAL_COSTGRAD, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, nullptr, ctx->d_scal + S_COST,
                   nullptr, P.R, nullptr, P.G, nullptr, P.rho, ctx->d_scal + S_EXTRA, false));
     return DRSDP_OK;
   }
   int hvp_at(Point &P, int p, const double *U, double *H) {
-    if (!fixed_mode()) return alm_hvp(ctx, p, P.M, s->ld, P.Y, s->ldp, U, P.G, s->K.ptr, P.rho, s->wZ.ptr, H);
+    if (!fixed_mode()) return alm_hvp(ctx, p, P.M, s->ld, P.Y, s->ldp, U, P.G, s->K.ptr, P.rho, s->wZ.ptr, H, s->Zbuf.ptr);
     return eval_fixed(ctx, DRSDP_EVAL_HVP, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, U, nullptr, nullptr, nullptr, H,
                       ctx->sub_G.ptr, s->K.ptr, P.rho, nullptr, true);
   }
@@ -283,11 +286,12 @@ struct Run {
     const int max_tcg = prm.max_tcg > 0 ? prm.max_tcg : std::max(1, n * (p - 1));
     iters_out = 0;
     tcg_out = 0;
+    // stagnation exit (reading R30): stop when the gradient norm has not halved within the last
+    // stall_rtr trust-region iterations
     double best_gn = s->cur.gn;
     int since_best = 0;
     for (int it = 0; it < prm.max_rtr; ++it) {
       if (s->cur.gn <= grad_tol) break;
-      // stagnation exit (reading R30): no halving of the gradient norm in stall_rtr iterations
       if (s->cur.gn <= 0.5 * best_gn) {
         best_gn = s->cur.gn;
         since_best = 0;
@@ -354,6 +358,7 @@ static void assign_points(SolverState *s) {
     pt.G = s->Gbuf[k].ptr;
     pt.rho = s->rhobuf[k].ptr;
     pt.yS = s->ySbuf[k].ptr;
+    pt.D = s->Dbuf[k].ptr;
   }
 }
 
@@ -409,7 +414,9 @@ static int alloc_solver(drsdp_ctx *ctx, int p0) {
     CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
     CK(s->rhobuf[k].ensure(P.n), "alloc");
     CK(s->ySbuf[k].ensure(P.m), "alloc");
+    if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Dbuf[k].ensure((size_t)P.n * P.ld), "alloc dense S");
   }
+  if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Zbuf.ensure((size_t)P.n * P.ld), "alloc dense Z");
   s->ldp = 0;
   RC(set_pitch(ctx, std::max(64, ((p0 + 63) / 64) * 64), false, 0));
   CK(s->wZ.ensure(P.m), "alloc");
@@ -650,7 +657,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
     int dv = 0;
     while (dv < prm.escape_max && dv < n && lam[dv] < thresh) ++dv;
-    // rank reduction (reading R15): compress Y to its numerical rank. Eigenpairs of the p x p
+    // rank reduction (readings R15, R32): compress Y to its numerical rank at the tolerance
+    // rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta_max))). Eigenpairs of the p x p
     // Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so row/column-major agree).
     {
       CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
@@ -660,13 +668,14 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
                            s->gwork.ptr, lw, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
         return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd (Gram)");
       ctx->launches++;
+      const double rtol = std::min(prm.rank_tol, std::max(1e-8, 0.01 * std::sqrt(eta_max)));
       std::vector<double> w(p), V((size_t)p * p);
       CK(cudaMemcpyAsync(w.data(), s->Gw.ptr, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
       CK(cudaMemcpyAsync(V.data(), s->Geig.ptr, sizeof(double) * p * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
       CK(cudaStreamSynchronize(ctx->stream), "sync");
       int r = 0;
       for (int i = 0; i < p; ++i)
-        if (w[i] > prm.rank_tol * prm.rank_tol * w[p - 1]) ++r;
+        if (w[i] > rtol * rtol * w[p - 1]) ++r;
       r = std::max(1, r);
       if (r < p) {
         // W_r = eigenvectors of the r largest eigenvalues (ascending order: the last r columns);

@@ -1,9 +1,7 @@
 mkdir -p gpurun_out
-run() { tag=$1; d=$2; tl=$3; shift; shift; shift; timeout $((tl+60)) python tools/solve_run.py $d $tl 4 "$@" > gpurun_out/exp_$tag.log 2>&1; echo "$tag d=$d $*: $(tail -1 gpurun_out/exp_$tag.log | cut -c1-300)"; }
-run J10 10 60 escape_max=8 rank_tol=1e-4 stall_rtr=5
-run J20 20 60 escape_max=8 rank_tol=1e-4 stall_rtr=5
-run J3 40 100 escape_max=8 rank_tol=1e-6 stall_rtr=5
-run J4 40 100 escape_max=8 rank_tol=1e-4 stall_rtr=10
-run J5 40 100 escape_max=3 rank_tol=1e-4 stall_rtr=5
-run J6 40 100 escape_max=8 rank_tol=1e-4 max_rtr=20
-run J100 100 500 escape_max=8 rank_tol=1e-4 stall_rtr=5
+run() { tag=$1; d=$2; tl=$3; p0=$4; shift 4; DRSDP_VERBOSE=1 timeout $((tl+90)) python tools/solve_run.py $d $tl $p0 "$@" > gpurun_out/exp_$tag.log 2> gpurun_out/exp_$tag.err; echo "$tag d=$d p0=$p0 $*: $(grep '"d"' gpurun_out/exp_$tag.log | cut -c1-260)"; }
+run P10 10 60 2
+run P20 20 60 2
+run P40 40 120 4
+run P40s1 40 120 4 seed=1
+run P100 100 420 16 escape_max=32
