@@ -83,15 +83,35 @@ int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
 // workspace / tile counters on demand and records the live timing events (kind 1..3) if enabled.
 int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind) {
   static const bool no_tma = std::getenv("DRSDP_NO_TMA") != nullptr;
+  // (small n keeps the register-direct gather kernel: one launch instead of assembly + product)
+  if (!no_tma && mode2 == MODE2_GATHER && !atr && a.n >= 2048 && (a.lda % 2) == 0 && ((uintptr_t)a.A & 15) == 0 &&
+      (a.k == 0 || a.k == a.n)) {
+    // gather-product on the TMA path: assemble W = A*(w) densely, then one K-concatenated product
+    // [M | W] [V; X] = M U + A*(w) Y, the Q of the HVP epilogue (Eq. 4.7's projection term)
+    const int64_t ldw = (a.n + 63) / 64 * 64;
+    CK(ctx->w_dense.ensure((size_t)a.n * ldw), "alloc dense A*(w)");
+    KL(gather_assemble_launch(a.n, a.amap, a.ldm, a.w, ctx->w_dense.ptr, ldw, a.skip, ctx->stream), "assemble A*(w)");
+    SymvArgs b = a;
+    b.A2 = ctx->w_dense.ptr;
+    b.lda2 = ldw;
+    b.V2 = a.X;
+    b.ldv2 = a.ldx;
+    b.amap = nullptr;
+    b.w = nullptr;
+    b.X = nullptr;
+    if (symv_tma_supported(b, epi, MODE2_PAIR, false)) return run_product(ctx, b, epi, MODE2_PAIR, false, prof_kind);
+  }
   if (!no_tma && symv_tma_supported(a, epi, mode2, atr)) {
     const int pt = symv_pt(a.p), bm = symv_tma_rows(), bk = symv_tma_kstep();
+    const bool pair = mode2 == MODE2_PAIR;
+    const int ktot = pair ? 2 * ((a.n + bk - 1) / bk * bk) : a.n;
     const int ntiles = ((a.n + bm - 1) / bm) * symv_chunks(a.p, epi);
     // split-K: one CTA per SM (the ring uses most of shared memory); waves x k-rows cost model
     int S = 1;
     double best = 1e300;
     for (int s = 1; s <= 64; ++s) {
-      const int per = ((a.n + s - 1) / s + bk - 1) / bk * bk;
-      if (s > 1 && (int64_t)(s - 1) * per >= a.n) break;
+      const int per = ((ktot + s - 1) / s + bk - 1) / bk * bk;
+      if (s > 1 && (int64_t)(s - 1) * per >= ktot) break;
       const int waves = (ntiles * s + ctx->num_sms - 1) / ctx->num_sms;
       const double cost = (double)waves * (per + 64) + 24.0 * s;
       if (cost < best * 0.999) {
@@ -99,12 +119,13 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
         S = s;
       }
     }
-    a.rows_per_split = ((a.n + S - 1) / S + bk - 1) / bk * bk;
+    a.rows_per_split = ((ktot + S - 1) / S + bk - 1) / bk * bk;
     if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bm * pt), "alloc split workspace");
     CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
     CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
     const int64_t ldvt = (a.n + 1) / 2 * 2;
-    CK(ctx->vt_buf.ensure((size_t)a.p * ldvt), "alloc V^T");
+    CK(ctx->vt_buf.ensure((size_t)(pair ? 2 : 1) * a.p * ldvt), "alloc V^T");
+    if (!pair) a.A2 = nullptr;
     a.part = ctx->symv_part.ptr;
     a.tile_cnt = ctx->tile_cnt.ptr;
     a.tile_scal = ctx->tile_scal.ptr;
@@ -742,6 +763,7 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->big_P.release();
   ctx->big_W.release();
   ctx->vt_buf.release();
+  ctx->w_dense.release();
   ctx->tile_cnt.release();
   ctx->tile_scal.release();
   ctx->sub_G.release();

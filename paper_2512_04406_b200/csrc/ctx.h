@@ -103,6 +103,7 @@ struct drsdp_ctx {
   drsdp::DBuf<double> symv_part;
   drsdp::DBuf<double> big_P, big_W;
   drsdp::DBuf<double> vt_buf;  // V^T staging for the TMA product kernel
+  drsdp::DBuf<double> w_dense;  // A*(w) assembled for the TMA gather-product
   const int *skip_flag = nullptr;  // set while device-resident tCG batches are being launched  // generic-p (> 64) product outputs, n x ldv
   drsdp::DBuf<unsigned> tile_cnt;
   drsdp::DBuf<double> tile_scal;

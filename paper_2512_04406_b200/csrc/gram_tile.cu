@@ -50,9 +50,11 @@ DRSDP_DEV void tma2d(void *dst, const CUtensorMap *m, int ci, int co, uint64_t *
       "l"(m), "r"(ci), "r"(co), "r"(su32(b))
       : "memory");
 }
-DRSDP_DEV double ldsw(const double *box, int row, int col) {
-  const char *b = reinterpret_cast<const char *>(box);
-  return *reinterpret_cast<const double *>(b + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3));
+DRSDP_DEV double ldsw(uint32_t box, int row, int col) {
+  const uint32_t a = box + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
 }
 }  // namespace
 
@@ -105,11 +107,11 @@ __global__ void __launch_bounds__(NT, 1)
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt % STAGES;
     bar_wait(&full[st], (kt / STAGES) & 1);
-    const double *sa = smem + st * STAGE_ELEMS, *sb = sa + OP_ELEMS;
+    const uint32_t sa = su32(smem) + st * STAGE_BYTES, sb = sa + OP_ELEMS * 8;
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       const int box = ks >> 2, col = ((ks & 3) << 2) + r;
-      const double *ba = sa + box * TB * 16, *bb = sb + box * TB * 16;
+      const uint32_t ba = sa + box * TB * 128, bb = sb + box * TB * 128;
       double af[JB], bf[CB];
 #pragma unroll
       for (int jb = 0; jb < JB; ++jb) af[jb] = ldsw(ba, wr * WM + 8 * jb + q, col);

@@ -855,6 +855,24 @@ __global__ void __launch_bounds__(256) tcg_finalize_kernel(int n, int p, int ld,
   }
 }
 
+// W = A*(w) as a dense matrix: W_ij = w[amap_ij] (0 where unconstrained); padding columns zeroed.
+// Feeds the gather-product A*(w) Y of Eq. 4.7's projection term to the TMA product kernel.
+__global__ void __launch_bounds__(256) gather_assemble_kernel(int n, const int32_t *__restrict__ amap, int64_t ldmap,
+                                                              const double *__restrict__ w, double *__restrict__ W,
+                                                              int64_t ldw, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
+  const int64_t total = (int64_t)n * ldw;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldw, j = e - i * ldw;
+    double v = 0.0;
+    if (j < n) {
+      const int32_t id = __ldg(amap + i * ldmap + j);
+      if (id >= 0) v = __ldg(w + id);
+    }
+    W[e] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 static inline int rows_grid(int64_t n) { return (int)((n + 7) / 8); }
 
@@ -980,6 +998,12 @@ cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *
   int nb = (int)(((size_t)n * ld + 255) / 256);
   if (nb > 1184) nb = 1184;
   tcg_finalize_kernel<<<nb, 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_assemble_launch(int n, const int32_t *amap, int64_t ldmap, const double *w, double *W, int64_t ldw,
+                                   const int *skip, cudaStream_t st) {
+  gather_assemble_kernel<<<1184, 256, 0, st>>>(n, amap, ldmap, w, W, ldw, skip);
   return cudaGetLastError();
 }
 

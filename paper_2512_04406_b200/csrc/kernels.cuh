@@ -152,6 +152,8 @@ cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const doub
 cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
                           unsigned *counter, double *out, cudaStream_t st);
 cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st);
+cudaError_t gather_assemble_launch(int n, const int32_t *amap, int64_t ldmap, const double *w, double *W, int64_t ldw,
+                                   const int *skip, cudaStream_t st);
 inline int rows_blocks(int64_t n) { return (int)((n + 7) / 8); }
 
 }  // namespace drsdp

@@ -61,9 +61,12 @@ DRSDP_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c_inner, int c
 
 // element (row, col) of a [rows][16] fp64 box written by TMA with SWIZZLE_128B (1024 B aligned):
 // the 16-byte chunk index (col / 2) is XORed with row % 8
-DRSDP_DEV double lds_sw(const double *box, int row, int col) {
-  const char *b = reinterpret_cast<const char *>(box);
-  return *reinterpret_cast<const double *>(b + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3));
+// (explicit ld.shared on a 32-bit shared address: a generic pointer would compile to LD.E)
+DRSDP_DEV double lds_sw(uint32_t box, int row, int col) {
+  const uint32_t a = box + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
 }
 
 template <int PT>
@@ -86,9 +89,13 @@ struct Cfg {
 
 }  // namespace
 
-template <int PT, int EPI>
+// PAIR: out = M V + A2 V2 as one K-concatenated product [M | A2] [V; V2]; the k-tiles in
+// [0, kpad) come from (tmA, tmV), those in [kpad, 2 kpad) from (tmA2, tmV2), kpad = n rounded up
+// to a multiple of BK (TMA zero-fills the padding columns).
+template <int PT, int EPI, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    symv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV, SymvArgs a) {
+    symv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
+                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmV2, SymvArgs a) {
   using C = Cfg<PT>;
   if (a.skip && *(volatile const int *)a.skip) return;
   extern __shared__ unsigned char smem_raw[];
@@ -102,8 +109,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int tile = blockIdx.x + gridDim.x * blockIdx.z;
   const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;
   const int j0 = blockIdx.x * BM;
+  const int kpad = (n + BK - 1) / BK * BK;
+  const int ktot = PAIR ? 2 * kpad : n;
   const int kbeg = split * a.rows_per_split;
-  const int kend = min(n, kbeg + a.rows_per_split);
+  const int kend = min(ktot, kbeg + a.rows_per_split);
   const int nk = (kend - kbeg + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -129,12 +138,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (kt >= C::STAGES) mbar_wait(&empty_bar[st], ((kt / C::STAGES) - 1) & 1);
         double *sa = smem + st * C::STAGE_ELEMS;
         double *sv = sa + C::A_ELEMS;
-        const int k0 = kbeg + kt * BK;
+        int k0 = kbeg + kt * BK;
+        const CUtensorMap *ma = &tmA, *mv = &tmV;
+        if (PAIR && k0 >= kpad) {
+          k0 -= kpad;
+          ma = &tmA2;
+          mv = &tmV2;
+        }
         mbar_arrive_expect_tx(&full_bar[st], C::STAGE_BYTES);
-        tma_load_2d(sa, &tmA, k0, j0, &full_bar[st]);
-        tma_load_2d(sa + BM * 16, &tmA, k0 + 16, j0, &full_bar[st]);
-        tma_load_2d(sv, &tmV, k0, c0, &full_bar[st]);
-        tma_load_2d(sv + PT * 16, &tmV, k0 + 16, c0, &full_bar[st]);
+        tma_load_2d(sa, ma, k0, j0, &full_bar[st]);
+        tma_load_2d(sa + BM * 16, ma, k0 + 16, j0, &full_bar[st]);
+        tma_load_2d(sv, mv, k0, c0, &full_bar[st]);
+        tma_load_2d(sv + PT * 16, mv, k0 + 16, c0, &full_bar[st]);
       }
     }
   } else {
@@ -146,12 +161,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int kt = 0; kt < nk; ++kt) {
       const int st = kt % C::STAGES;
       mbar_wait(&full_bar[st], (kt / C::STAGES) & 1);
-      const double *sa = smem + st * C::STAGE_ELEMS;
-      const double *sv = sa + C::A_ELEMS;
+      const uint32_t sa = smem_u32(smem) + st * C::STAGE_BYTES;
+      const uint32_t sv = sa + C::A_ELEMS * 8;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         const int box = ks >> 2, col = ((ks & 3) << 2) + r;
-        const double *ba = sa + box * BM * 16, *bv = sv + box * PT * 16;
+        const uint32_t ba = sa + box * BM * 128, bv = sv + box * PT * 128;
         double af[C::JB], bf[C::CB];
 #pragma unroll
         for (int jb = 0; jb < C::JB; ++jb) af[jb] = lds_sw(ba, arow + 8 * jb, col);
@@ -398,7 +413,8 @@ static bool make_map(CUtensorMap *m, const double *base, int64_t rows, int64_t c
 }
 
 bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
-  if (mode2 != MODE2_NONE || atr || (a.k > 0 && a.k != a.n)) return false;
+  if (mode2 == MODE2_GATHER || atr || (a.k > 0 && a.k != a.n)) return false;
+  if (mode2 == MODE2_PAIR && ((a.lda2 & 1) || ((uintptr_t)a.A2 & 15))) return false;
   if (epi != EPI_RAW && a.p > 64) return false;
   if ((a.lda & 1) || ((uintptr_t)a.A & 15)) return false;
   return encode_fn() != nullptr;
@@ -407,11 +423,10 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
 int symv_tma_rows() { return BM; }
 int symv_tma_kstep() { return BK; }
 
-template <int PT, int EPI>
-static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap &mA, const CUtensorMap &mV, int S,
-                                cudaStream_t st) {
+template <int PT, int EPI, bool PAIR>
+static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap *m, int S, cudaStream_t st) {
   using C = Cfg<PT>;
-  auto k = symv_tma_kernel<PT, EPI>;
+  auto k = symv_tma_kernel<PT, EPI, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
@@ -420,36 +435,55 @@ static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap &mA, const 
   }
   const int nz = EPI == EPI_RAW ? (a.p + PT - 1) / PT : 1;
   dim3 grid((a.n + BM - 1) / BM, S, nz);
-  k<<<grid, NTHREADS, C::SMEM_BYTES, st>>>(mA, mV, a);
+  k<<<grid, NTHREADS, C::SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], a);
   return cudaGetLastError();
 }
 
 template <int PT>
-static cudaError_t tma_dispatch(const SymvArgs &a, int epi, const CUtensorMap &mA, const CUtensorMap &mV, int S,
+static cudaError_t tma_dispatch(const SymvArgs &a, int epi, bool pair, const CUtensorMap *m, int S,
                                 cudaStream_t st) {
+  if (pair) {
+    if (epi == EPI_RAW) return tma_launch_t<PT, EPI_RAW, true>(a, m, S, st);
+    if (epi == EPI_HVP) return tma_launch_t<PT, EPI_HVP, true>(a, m, S, st);
+    return cudaErrorInvalidValue;
+  }
   switch (epi) {
-    case EPI_RAW: return tma_launch_t<PT, EPI_RAW>(a, mA, mV, S, st);
-    case EPI_COSTGRAD: return tma_launch_t<PT, EPI_COSTGRAD>(a, mA, mV, S, st);
-    case EPI_HVP: return tma_launch_t<PT, EPI_HVP>(a, mA, mV, S, st);
-    default: return tma_launch_t<PT, EPI_ROWDOT>(a, mA, mV, S, st);
+    case EPI_RAW: return tma_launch_t<PT, EPI_RAW, false>(a, m, S, st);
+    case EPI_COSTGRAD: return tma_launch_t<PT, EPI_COSTGRAD, false>(a, m, S, st);
+    case EPI_HVP: return tma_launch_t<PT, EPI_HVP, false>(a, m, S, st);
+    default: return tma_launch_t<PT, EPI_ROWDOT, false>(a, m, S, st);
   }
 }
 
-// Vt: workspace of at least round_up(p, PT) * ldvt doubles, ldvt = round_up(n, 2)
+// Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR), ldvt = round_up(n, 2)
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st) {
   const int pt = symv_pt(a.p);
+  const bool pair = a.A2 != nullptr;
   dim3 tg((a.n + 31) / 32, (a.p + 31) / 32);
   transpose_kernel<<<tg, 256, 0, st>>>(a.n, a.p, a.V, a.ldv, Vt, ldvt, a.skip);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  CUtensorMap mA, mV;
-  if (!make_map(&mA, a.A, a.n, a.n, a.lda, BM) || !make_map(&mV, Vt, a.p, a.n, ldvt, pt))
+  double *Vt2 = Vt + (size_t)a.p * ldvt;
+  if (pair) {
+    transpose_kernel<<<tg, 256, 0, st>>>(a.n, a.p, a.V2, a.ldv2, Vt2, ldvt, a.skip);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  CUtensorMap m[4];
+  if (!make_map(&m[0], a.A, a.n, a.n, a.lda, BM) || !make_map(&m[1], Vt, a.p, a.n, ldvt, pt))
     return cudaErrorInvalidValue;
+  if (pair) {
+    if (!make_map(&m[2], a.A2, a.n, a.n, a.lda2, BM) || !make_map(&m[3], Vt2, a.p, a.n, ldvt, pt))
+      return cudaErrorInvalidValue;
+  } else {
+    m[2] = m[0];
+    m[3] = m[1];
+  }
   switch (pt) {
-    case 8: return tma_dispatch<8>(a, epi, mA, mV, S, st);
-    case 16: return tma_dispatch<16>(a, epi, mA, mV, S, st);
-    case 32: return tma_dispatch<32>(a, epi, mA, mV, S, st);
-    default: return tma_dispatch<64>(a, epi, mA, mV, S, st);
+    case 8: return tma_dispatch<8>(a, epi, pair, m, S, st);
+    case 16: return tma_dispatch<16>(a, epi, pair, m, S, st);
+    case 32: return tma_dispatch<32>(a, epi, pair, m, S, st);
+    default: return tma_dispatch<64>(a, epi, pair, m, S, st);
   }
 }
 

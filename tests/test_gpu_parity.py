@@ -244,6 +244,37 @@ def test_alm_eval_parity(ctx, d, seed, sigma, p):
     assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
 
 
+@pytest.mark.parametrize("d,p", [(40, 24), (100, 40), (100, 96)])
+def test_alm_eval_full_size(ctx, d, p):
+    """BASELINE configs[1]/[2] sizes (n = 821, 5051): the y-eliminated evaluation in the solver's
+    launch configuration (dense Gram tiles + TMA products, pitch 64) against the oracle."""
+    from paper_2512_04406_b200 import abi
+
+    Q, c, amap, cnt, b, T, Y, U = _state(d, 7, 3.0, p)
+    n = amap.shape[0]
+    sigma = 3.0
+    ctx.set_bqp(Q, c)
+    ld = n + (-n) % 64
+    Tpad = np.zeros((n, ld))
+    Tpad[:, :n] = T
+    Td = dev(Tpad)
+    # the ABI takes pitch p (even p: the TMA / dense-Gram path)
+    Yd, Ud = dev(Y), dev(U)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    E, R, H = torch.empty_like(Yd), torch.empty_like(Yd), torch.empty_like(Yd)
+    ctx.alm_eval(abi.EVAL_COSTGRAD | abi.EVAL_HVP, p, Td, ld, sigma, Yd, Ud, cost, E, R, H)
+    torch.cuda.synchronize()
+    o = sp.alm_eval(T, amap, cnt, None, sigma, Y, U)
+    G = Y.T @ Y
+    sE = np.linalg.norm(4 * o["M"] @ Y) + np.linalg.norm(4 * Y @ G)
+    m0 = np.sum((T / sigma) ** 2)
+    assert abs(cost.item() - o["f"]) <= TOL * (np.sum(G * G) + m0 + np.sum(o["y"] ** 2 * cnt))
+    assert rel(E.cpu().numpy(), o["E"], sE) <= TOL
+    assert rel(R.cpu().numpy(), o["R"], sE) <= TOL
+    sH = sE + np.linalg.norm(4 * ops.At(amap, ops.A(amap, Y @ U.T + U @ Y.T, cnt.size) / cnt) @ Y)
+    assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
+
+
 @pytest.mark.parametrize("d,p", [(6, 3), (12, 7), (14, 70)])
 def test_operator_kernels(ctx, d, p):
     """(a) assembly, (d) y-update and dual update against the oracle's plain definitions."""
