@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *_
   double g2 = 0.0;
   for (int e = threadIdx.x; e < nval; e += blockDim.x) {
     double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(part + (size_t)b * nval + e);
+    s = ordered_sum(part + e, (int)gridDim.x, (size_t)nval);
     if (e < pp) {
       G[e] = s;
       g2 += s * s;
@@ -747,36 +747,33 @@ __global__ void tcg_init_kernel(TcgDev *st, double gnorm, double Delta, int max_
   st->max_iters = max_iters;
 }
 
-__global__ void tcg_decide_kernel(TcgDev *st, const double *kappa) {
-  if (threadIdx.x || st->done) return;
-  const double dHd = *kappa;
-  st->iters += 1;
-  if (!isfinite(dHd)) {
-    st->done = 2;
-    return;
-  }
-  const double alpha = dHd != 0.0 ? st->r_r / dHd : INFINITY;
-  const double e_Pe_new = st->e_Pe + 2.0 * alpha * st->e_Pd + alpha * alpha * st->d_Pd;
-  if (dHd <= 0.0 || e_Pe_new >= st->Delta2) {
-    st->alpha = (-st->e_Pd + sqrt(st->e_Pd * st->e_Pd + st->d_Pd * (st->Delta2 - st->e_Pe))) / st->d_Pd;
-    st->boundary = 1;
-  } else {
-    st->alpha = alpha;
-    st->boundary = 0;
-    st->e_Pe_new = e_Pe_new;
-  }
-}
-
-// dots: [<eta', g>, <eta', H eta'>, <r', r'>]
+// One tCG iteration after H delta is known (oracle/rtr.py tcg, lines "d_Hd = ..." to the new
+// direction): every block derives the same step (alpha, or the boundary step tau) from kappa =
+// <delta, H delta> and the device scalars, updates its rows (ping-pong buffers), and the last
+// block applies the acceptance / stopping rules. With use_cond it also drives the conditional
+// WHILE node of the captured graph (keep looping while the tCG runs).
 __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, TcgDev *st, double *e0, double *e1,
                                                          double *h0, double *h1, double *r0, double *r1,
                                                          const double *__restrict__ d, const double *__restrict__ hd,
                                                          const double *__restrict__ g, double *part,
-                                                         unsigned *counter) {
+                                                         unsigned *counter, const double *kappa,
+                                                         cudaGraphConditionalHandle cond, int use_cond) {
   if (*(volatile const int *)&st->done) return;
   __shared__ double scratch[3 * 8];
-  const int par = st->par, bnd = st->boundary;
-  const double a = st->alpha;
+  const double dHd = *(volatile const double *)kappa;
+  if (!isfinite(dHd)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->done = 2;
+      if (use_cond) cudaGraphSetConditional(cond, 0u);
+    }
+    return;
+  }
+  const double r_r = st->r_r, e_Pe = st->e_Pe, e_Pd = st->e_Pd, d_Pd = st->d_Pd, Delta2 = st->Delta2;
+  const double alpha = dHd != 0.0 ? r_r / dHd : INFINITY;
+  const double e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd;
+  const int bnd = (dHd <= 0.0 || e_Pe_new >= Delta2) ? 1 : 0;
+  const double a = bnd ? (-e_Pd + sqrt(e_Pd * e_Pd + d_Pd * (Delta2 - e_Pe))) / d_Pd : alpha;
+  const int par = st->par;
   const double *e = par ? e1 : e0, *h = par ? h1 : h0, *r = par ? r1 : r0;
   double *eo = par ? e0 : e1, *ho = par ? h0 : h1, *ro = par ? r0 : r1;
   double v[3] = {0.0, 0.0, 0.0};
@@ -799,31 +796,34 @@ __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, T
   }
   ROW_LOOP_END
   if (!grid_sum<3>(v, part, counter, nullptr, scratch) || threadIdx.x != 0) return;
+  st->iters += 1;
+  st->alpha = a;
+  st->boundary = bnd;
   if (bnd) {
     st->par = 1 - par;
     st->hit = 1;
     st->done = 1;
-    return;
+  } else {
+    const double new_model = v[0] + 0.5 * v[1];
+    if (new_model >= st->model) {  // no model decrease: keep the previous eta (oracle/rtr.py)
+      st->done = 1;
+    } else {
+      st->par = 1 - par;
+      st->model = new_model;
+      st->e_Pe = e_Pe_new;
+      st->r_r = v[2];
+      if (sqrt(v[2]) <= st->norm_r0 * fmin(st->norm_r0, 0.1)) {  // theta = 1, kappa = 0.1
+        st->done = 1;
+      } else {
+        const double beta = v[2] / r_r;
+        st->e_Pd = beta * (e_Pd + a * d_Pd);
+        st->d_Pd = v[2] + beta * beta * d_Pd;
+        st->beta = beta;
+        if (st->iters >= st->max_iters) st->done = 1;
+      }
+    }
   }
-  const double new_model = v[0] + 0.5 * v[1];
-  if (new_model >= st->model) {  // no model decrease: keep the previous eta (oracle/rtr.py)
-    st->done = 1;
-    return;
-  }
-  st->par = 1 - par;
-  st->model = new_model;
-  st->e_Pe = st->e_Pe_new;
-  const double r_r_old = st->r_r;
-  st->r_r = v[2];
-  if (sqrt(v[2]) <= st->norm_r0 * fmin(st->norm_r0, 0.1)) {  // theta = 1, kappa = 0.1
-    st->done = 1;
-    return;
-  }
-  const double beta = v[2] / r_r_old;
-  st->e_Pd = beta * (st->e_Pd + a * st->d_Pd);
-  st->d_Pd = v[2] + beta * beta * st->d_Pd;
-  st->beta = beta;
-  if (st->iters >= st->max_iters) st->done = 1;
+  if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, const TcgDev *st,
@@ -839,10 +839,6 @@ __global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, c
   s = warp_sum(s);
   for (int c = lane; c < p; c += 32) d[o + c] = fma(beta, d[o + c], -r[o + c]) - s * Y[o + c];
   ROW_LOOP_END
-}
-
-__global__ void tcg_cond_kernel(cudaGraphConditionalHandle h, const TcgDev *st) {
-  if (threadIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(256) tcg_finalize_kernel(int n, int p, int ld, const TcgDev *st, double *e0,
@@ -972,14 +968,12 @@ cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iter
   tcg_init_kernel<<<1, 32, 0, s>>>(st, gnorm, Delta, max_iters);
   return cudaGetLastError();
 }
-cudaError_t tcg_decide_launch(TcgDev *st, const double *kappa, cudaStream_t s) {
-  tcg_decide_kernel<<<1, 32, 0, s>>>(st, kappa);
-  return cudaGetLastError();
-}
 cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
                               double *r0, double *r1, const double *d, const double *hd, const double *g,
-                              double *part, unsigned *counter, cudaStream_t s) {
-  tcg_update_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1, r0, r1, d, hd, g, part, counter);
+                              double *part, unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond,
+                              int use_cond, cudaStream_t s) {
+  tcg_update_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1, r0, r1, d, hd, g, part, counter,
+                                                 kappa, cond, use_cond);
   return cudaGetLastError();
 }
 cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
@@ -988,10 +982,6 @@ cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const doub
   return cudaGetLastError();
 }
 
-cudaError_t tcg_cond_launch(cudaGraphConditionalHandle h, const TcgDev *st, cudaStream_t s) {
-  tcg_cond_kernel<<<1, 32, 0, s>>>(h, st);
-  return cudaGetLastError();
-}
 cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *e0, const double *e1, double *h0,
                                 const double *h1, cudaStream_t s) {
   (void)p;

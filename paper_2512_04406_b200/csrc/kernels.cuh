@@ -134,15 +134,13 @@ struct TcgDev {
   int max_iters;
 };
 cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, cudaStream_t s);
-// after H delta: kappa = <delta, H delta> (device scalar) -> alpha or the boundary step tau
-cudaError_t tcg_decide_launch(TcgDev *st, const double *kappa, cudaStream_t s);
+// after H delta: kappa = <delta, H delta> (device scalar) -> alpha or the boundary step tau;
 // eta' = eta + alpha delta, (H eta)' = H eta + alpha H delta, r' = r + alpha H delta, then the
-// model / residual decisions (last block)
+// model / residual decisions (last block); use_cond: also set the graph's WHILE condition
 cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
                               double *r0, double *r1, const double *d, const double *hd, const double *g,
-                              double *part, unsigned *counter, cudaStream_t s);
-// conditional-while body terminator: keep looping while the tCG is running
-cudaError_t tcg_cond_launch(cudaGraphConditionalHandle h, const TcgDev *st, cudaStream_t s);
+                              double *part, unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond,
+                              int use_cond, cudaStream_t s);
 // move the result into buffer 0 (eta, H eta) when it ended in buffer 1
 cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *e0, const double *e1, double *h0,
                                 const double *h1, cudaStream_t s);

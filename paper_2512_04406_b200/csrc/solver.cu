@@ -150,18 +150,18 @@ struct Run {
   void swap_pts() { std::swap(s->cur, s->prop); }
 
   // Steihaug-Toint truncated CG (oracle/rtr.py tcg), device-resident: the scalar recurrences run
-  // in tcg_decide / tcg_update (kernels.cu). The loop body (HVP, decide, update, new direction)
+  // in tcg_update (kernels.cu). The loop body (HVP, update + stopping rules, new direction)
   // is captured once per (current point, p) into a CUDA graph whose conditional WHILE node
   // repeats it until the device flag `done` is set, so a whole tCG runs from one graph launch
   // with no host round trip. The result is left in s->eta / s->Heta and the scalars in
   // s->tcg (read back with the trust-region step's synchronisation).
-  int tcg_body(int p) {
+  int tcg_body(int p, cudaGraphConditionalHandle cond, int use_cond) {
     Point &C = s->cur;
     TcgDev *st = s->tcg.ptr;
     RC(hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr));
-    KL(tcg_decide_launch(st, ctx->d_scal + S_SCAL, ctx->stream), "tcg decide");
     KL(tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr, s->r.ptr, s->r2.ptr,
-                         s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC, ctx->stream),
+                         s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
+                         ctx->d_scal + S_SCAL, cond, use_cond, ctx->stream),
        "tcg update");
     KL(tcg_newdir_launch(n, p, s->ldp, st, C.Y, s->r.ptr, s->r2.ptr, s->delta.ptr, ctx->stream), "tcg newdir");
     return DRSDP_OK;
@@ -183,8 +183,7 @@ struct Run {
                                      cudaStreamCaptureModeRelaxed),
        "begin capture");
     ctx->skip_flag = &s->tcg.ptr->done;
-    int rc = tcg_body(p);
-    if (rc == DRSDP_OK) rc = cuda_check(ctx, tcg_cond_launch(h, s->tcg.ptr, ctx->stream), "tcg cond");
+    int rc = tcg_body(p, h, 1);
     ctx->skip_flag = nullptr;
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &body_out);
     if (rc) {
@@ -233,7 +232,7 @@ struct Run {
       for (;;) {
         ctx->skip_flag = &st->done;
         for (int b = 0; b < batch; ++b) {
-          int rc = tcg_body(p);
+          int rc = tcg_body(p, cudaGraphConditionalHandle{}, 0);
           if (rc) {
             ctx->skip_flag = nullptr;
             return rc;
@@ -318,7 +317,7 @@ struct Run {
       const bool hit = s->h_tcg->hit != 0;
       tcg_out += nin;
       hvp += nin;
-      ctx->launches += (int64_t)nin * 6;
+      ctx->launches += (int64_t)nin * 5;
       const double d3[2] = {ctx->h_scal[S_DOTS], ctx->h_scal[S_DOTS + 1]};
       if (flag) {
         Delta /= 4.0;

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
     for (int e = 0; e < EPT; ++e) {
       const int idx = threadIdx.x + 256 * e;
       double s = 0.0;
-      for (int k = 0; k < S; ++k) s += __ldcg(rp + (size_t)k * TILE + idx);
+      s = ordered_sum(rp + idx, S, (size_t)TILE);
       ptile[idx] = s;
     }
     if (threadIdx.x == 0) a.tile_cnt[tile] = 0u;
@@ -288,12 +288,15 @@ __global__ void __launch_bounds__(256, 2) symv_kernel(SymvArgs a) {
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
+  // tile scalars: thread t sums tiles t, t + blockDim, ... then a fixed-order block reduction
+  double tv[2] = {0.0, 0.0};
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+    tv[0] += __ldcg(a.tile_scal + 2 * t);
+    tv[1] += __ldcg(a.tile_scal + 2 * t + 1);
+  }
+  block_sum<2>(tv, scratch);
   if (threadIdx.x == 0) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int t = 0; t < (int)gridDim.x; ++t) {
-      t0 += __ldcg(a.tile_scal + 2 * t);
-      t1 += __ldcg(a.tile_scal + 2 * t + 1);
-    }
+    const double t0 = tv[0], t1 = tv[1];
     if (a.scal_out) {
       a.scal_out[0] = t0;
       a.scal_out[1] = t1;

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const double *rp = a.part + (size_t)tile * S * C::TILE;
     for (int e = threadIdx.x; e < C::TILE; e += NTHREADS) {
       double sum = 0.0;
-      for (int k = 0; k < S; ++k) sum += __ldcg(rp + (size_t)k * C::TILE + e);
+      sum = ordered_sum(rp + e, S, (size_t)C::TILE);
       ptile[e] = sum;
     }
     if (threadIdx.x == 0) a.tile_cnt[tile] = 0u;
@@ -342,12 +342,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
+  // tile scalars: thread t sums tiles t, t + blockDim, ... then a fixed-order block reduction
+  double tv[2] = {0.0, 0.0};
+  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
+    tv[0] += __ldcg(a.tile_scal + 2 * t);
+    tv[1] += __ldcg(a.tile_scal + 2 * t + 1);
+  }
+  block_sum<2>(tv, scratch);
   if (threadIdx.x == 0) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int t = 0; t < (int)gridDim.x; ++t) {
-      t0 += __ldcg(a.tile_scal + 2 * t);
-      t1 += __ldcg(a.tile_scal + 2 * t + 1);
-    }
+    const double t0 = tv[0], t1 = tv[1];
     if (a.scal_out) {
       a.scal_out[0] = t0;
       a.scal_out[1] = t1;
