@@ -115,7 +115,8 @@ typedef struct {
   double eps_scale, eps_floor;         /* inner tolerance eps_k = max(0.1 min(1,eta) eps_scale, eps_floor) on ||XY|| */
   double time_limit_s;                 /* 0 = none                                                */
   int32_t p0;                          /* initial factorization size                      */
-  int32_t max_outer, max_rtr, max_tcg; /* iteration caps (max_tcg <= 0: n(p-1))                   */
+  int32_t max_outer, max_rtr, max_tcg; /* iteration caps (max_tcg: truncated-CG cap, default 100,
+                                          <= 0: the manifold dimension n(p-1); reading R33)       */
   int32_t escape_max;                  /* at most this many escape eigenvectors per iteration     */
   int32_t mode;                        /* 0 = y-eliminated ALM subproblem (default), 1 = fixed-M  */
   uint64_t seed;                       /* Y^0 draw when no initial factor is given                */

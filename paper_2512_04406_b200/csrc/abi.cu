@@ -531,8 +531,22 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
             const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf) {
   Problem &P = ctx->prob;
   const int n = (int)P.n;
+  // K = U^T Y + Y^T U runs on the auxiliary stream, concurrently with Z and its segmented sum
+  // (fork / join with events; inside a graph capture this becomes two parallel branches)
+  cudaStream_t main_stream = ctx->stream;
+  const bool fork = ctx->aux_stream != nullptr;
+  if (fork) {
+    CK(cudaEventRecord(ctx->ev_fork, main_stream), "event record");
+    CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0), "stream wait");
+    ctx->stream = ctx->aux_stream;
+  }
   int rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, U, nullptr, K, nullptr)
                   : gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
+  if (fork) {
+    ctx->stream = main_stream;
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev_join, ctx->aux_stream), "event record");
+  }
   if (rc) return rc;
   SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
   if (Zbuf && use_dense(Y, U, ldv)) {
@@ -542,6 +556,7 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
     s.ldd = P.ld;
   }
   KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
+  if (fork) CK(cudaStreamWaitEvent(main_stream, ctx->ev_join, 0), "stream wait");
   if (p > 64) return hvp_generic(ctx, n, p, M, ldm, Y, ldv, U, G, K, rho, P.amap.ptr, P.ld, wZ, hvp);
   SymvArgs a = base_symv(ctx, n, p, M, ldm);
   a.V = U;
@@ -736,6 +751,13 @@ int drsdp_create(drsdp_ctx **out, int device, void *cuda_stream) {
     drsdp_destroy(ctx);
     return DRSDP_ERR_CUDA;
   }
+  if (cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    drsdp_destroy(ctx);
+    return DRSDP_ERR_CUDA;
+  }
   drsdp_default_params(&ctx->prm);
   *out = ctx;
   return DRSDP_OK;
@@ -784,6 +806,12 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   if (ctx->h_scal) cudaFreeHost(ctx->h_scal);
   if (ctx->d_flag) cudaFree(ctx->d_flag);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->aux_stream) {
+    cudaStreamSynchronize(ctx->aux_stream);
+    cudaStreamDestroy(ctx->aux_stream);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -961,7 +989,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->p0 = 2;
   o->max_outer = 300;
   o->max_rtr = 500;
-  o->max_tcg = 0;
+  o->max_tcg = 100;
   o->escape_max = 8;
   o->mode = 0;
   o->seed = 0;

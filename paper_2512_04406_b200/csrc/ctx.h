@@ -88,6 +88,8 @@ struct drsdp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t aux_stream = nullptr;  // concurrent branch inside an evaluation (K next to Z)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   int sticky = 0;
   int64_t launches = 0;

@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python tools/solve_run.py 10,20,40 120 > gpurun_out/solve_rep.log 2>&1; grep '"d"' gpurun_out/solve_rep.log | cut -c1-230
-timeout 200 python tools/quick_sweep.py 16384,32768 16,64 > gpurun_out/sweep_tma.log 2>&1; cut -c1-140 gpurun_out/sweep_tma.log
+bash tools/gpu_profile.sh
+run() { tag=$1; d=$2; tl=$3; p0=$4; shift 4; timeout $((tl+90)) python tools/solve_run.py $d $tl $p0 "$@" > gpurun_out/exp_$tag.log 2> gpurun_out/exp_$tag.err; echo "$tag d=$d p0=$p0 $*: $(grep '"d"' gpurun_out/exp_$tag.log | cut -c1-200)"; }
+run T1 40 120 4 max_tcg=100
+run T2 40 120 4 max_tcg=300
+run T3 40 120 4 max_tcg=1000
