@@ -101,6 +101,35 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     b.X = nullptr;
     if (symv_tma_supported(b, epi, MODE2_PAIR, false)) return run_product(ctx, b, epi, MODE2_PAIR, false, prof_kind);
   }
+  static const bool no_symm = std::getenv("DRSDP_NO_SYMM") != nullptr;
+  if (!no_tma && !no_symm && a.n >= 4096 && symm_supported(a, epi, mode2, atr)) {
+    // upper-triangle product: reads the distinct entries of M only (symv_symm.cu)
+    if (ctx->symm_n != a.n) {
+      std::vector<int> hu, hs;
+      const int nu = symm_units(a.n, hu, hs);
+      CK(ctx->symm_units.ensure((size_t)nu), "alloc unit table");
+      CK(cudaMemcpy(ctx->symm_units.ptr, hu.data(), sizeof(int) * hu.size(), cudaMemcpyHostToDevice), "copy units");
+      CK(ctx->symm_ustart.ensure(hs.size()), "alloc unit starts");
+      CK(cudaMemcpy(ctx->symm_ustart.ptr, hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice), "copy starts");
+      ctx->symm_n = a.n;
+      ctx->symm_nunits = nu;
+    }
+    const int nb = (a.n + 127) / 128;
+    CK(ctx->symm_F.ensure(symm_fpart_elems(ctx->symm_nunits, 16)), "alloc forward partials");
+    CK(ctx->symm_T.ensure(symm_tpart_elems(a.n, 16)), "alloc transposed partials");
+    CK(ctx->tile_scal.ensure((size_t)nb * 2 * 4), "alloc tile scalars");
+    const int64_t ldvt = (a.n + 1) / 2 * 2;
+    CK(ctx->vt_buf.ensure((size_t)a.p * ldvt), "alloc V^T");
+    a.tile_scal = ctx->tile_scal.ptr;
+    a.glob_cnt = ctx->counters + C_SYMV;
+    int rc = prof_kind ? prof_begin(ctx, prof_kind) : DRSDP_OK;
+    if (rc) return rc;
+    ctx->launches += 2;  // transpose + partial kernel (+ the reduce below)
+    KL(symm_launch(a, epi, ctx->vt_buf.ptr, ldvt, ctx->symm_units.ptr, ctx->symm_nunits, ctx->symm_ustart.ptr,
+                   ctx->symm_F.ptr, ctx->symm_T.ptr, ctx->stream),
+       "product kernel (upper triangle)");
+    return prof_kind ? prof_end(ctx) : DRSDP_OK;
+  }
   if (!no_tma && symv_tma_supported(a, epi, mode2, atr)) {
     const int pt = symv_pt(a.p), bm = symv_tma_rows(), bk = symv_tma_kstep();
     const bool pair = mode2 == MODE2_PAIR;
@@ -786,6 +815,10 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->big_W.release();
   ctx->vt_buf.release();
   ctx->w_dense.release();
+  ctx->symm_units.release();
+  ctx->symm_ustart.release();
+  ctx->symm_F.release();
+  ctx->symm_T.release();
   ctx->tile_cnt.release();
   ctx->tile_scal.release();
   ctx->sub_G.release();

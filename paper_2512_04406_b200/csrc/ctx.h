@@ -106,6 +106,11 @@ struct drsdp_ctx {
   drsdp::DBuf<double> big_P, big_W;
   drsdp::DBuf<double> vt_buf;  // V^T staging for the TMA product kernel
   drsdp::DBuf<double> w_dense;  // A*(w) assembled for the TMA gather-product
+  // symmetric-half product (symv_symm.cu): unit table for symm_n, partial buffers
+  int symm_n = 0, symm_nunits = 0;
+  drsdp::DBuf<int4> symm_units;
+  drsdp::DBuf<int> symm_ustart;
+  drsdp::DBuf<double> symm_F, symm_T;
   const int *skip_flag = nullptr;  // set while device-resident tCG batches are being launched  // generic-p (> 64) product outputs, n x ldv
   drsdp::DBuf<unsigned> tile_cnt;
   drsdp::DBuf<double> tile_scal;

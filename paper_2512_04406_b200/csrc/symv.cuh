@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace drsdp {
 
 enum Epi { EPI_RAW = 0, EPI_COSTGRAD = 1, EPI_HVP = 2, EPI_ROWDOT = 3 };
@@ -73,5 +75,19 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr);
 int symv_tma_rows();
 int symv_tma_kstep();
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st);
+// Vt (p x ldvt) = V^T for a k x p row-major V (pitch ldv)
+cudaError_t symv_transpose(int k, int p, const double *V, int ldv, double *Vt, int64_t ldvt, const int *skip,
+                           cudaStream_t st);
+
+// Upper-triangle ("symmetric half") variant (symv_symm.cu) for p <= 16: a partial-product kernel
+// over runs of 128 x 128 upper tiles and a reduce + row-epilogue kernel (one CTA per 128 rows).
+// symm_units fills the unit table (int4 {I, Ja, Jb, 0} per unit) and the per-block-row start
+// offsets (nb + 1), returning the unit count.
+bool symm_supported(const SymvArgs &a, int epi, int mode2, bool atr);
+int symm_units(int n, std::vector<int> &host_units, std::vector<int> &host_ustart);
+size_t symm_tpart_elems(int n, int p);
+size_t symm_fpart_elems(int n_units, int p);
+cudaError_t symm_launch(const SymvArgs &a, int epi, double *Vt, int64_t ldvt, const int4 *units, int n_units,
+                        const int *ustart, double *Fpart, double *Tpart, cudaStream_t st);
 
 }  // namespace drsdp

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "symv.cuh"
+#include "tile_epilogue.cuh"
 
 namespace drsdp {
 
@@ -218,148 +219,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncthreads();
   }
 
-  // ---- row epilogue on the finished tile (warp per row, lanes over columns) ----
-  constexpr int CPL = (PT + 31) / 32;
-  if constexpr (EPI == EPI_COSTGRAD || EPI == EPI_HVP) {
-    for (int t = threadIdx.x; t < p * p; t += NTHREADS) gs[t] = a.G[t];
-    if constexpr (EPI == EPI_HVP)
-      for (int t = threadIdx.x; t < p * p; t += NTHREADS) gs[p * p + t] = a.K[t];
-  }
-  __syncthreads();
-  double sc0 = 0.0, sc1 = 0.0;
-  for (int jj = warp; jj < BM; jj += NCW + 1) {
-    const int j = j0 + jj;
-    if (j >= n) break;
-    double pv[CPL], yv[CPL];
-#pragma unroll
-    for (int h = 0; h < CPL; ++h) {
-      const int c = lane + 32 * h;
-      pv[h] = (c < p) ? ptile[jj * PT + c] : 0.0;
-      yv[h] = 0.0;
-      if constexpr (EPI != EPI_RAW) yv[h] = (c < p) ? a.Y[(size_t)j * a.ldy + c] : 0.0;
-    }
-    if constexpr (EPI == EPI_RAW) {
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        const int c = lane + 32 * h;
-        if (c < p) a.out[(size_t)j * a.ldo + c0 + c] = pv[h];
-      }
-    } else if constexpr (EPI == EPI_ROWDOT) {
-      double d = 0.0;
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) d += pv[h] * yv[h];
-      d = warp_sum(d);
-      if (lane == 0) a.zout[j] = d;
-      sc0 += (lane == 0) ? d : 0.0;
-    } else if constexpr (EPI == EPI_COSTGRAD) {
-      double yg[CPL];
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) yg[h] = 0.0;
-      for (int k = 0; k < p; ++k) {
-        const double yk = __shfl_sync(0xffffffffu, yv[k >> 5], k & 31);
-#pragma unroll
-        for (int h = 0; h < CPL; ++h) {
-          const int c = lane + 32 * h;
-          if (c < p) yg[h] = fma(yk, gs[k * p + c], yg[h]);
-        }
-      }
-      double e[CPL], py = 0.0, ey = 0.0;
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        e[h] = 4.0 * (yg[h] - pv[h]);
-        py += pv[h] * yv[h];
-        ey += e[h] * yv[h];
-      }
-      py = warp_sum(py);
-      const double rho = warp_sum(ey);
-      double rr = 0.0;
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        const int c = lane + 32 * h;
-        const double rv = e[h] - rho * yv[h];
-        rr += rv * rv;
-        if (c < p) {
-          if (a.out) a.out[(size_t)j * a.ldo + c] = rv;
-          if (a.egrad) a.egrad[(size_t)j * a.lde + c] = e[h];
-        }
-      }
-      rr = warp_sum(rr);
-      if (lane == 0) {
-        if (a.rho_out) a.rho_out[j] = rho;
-        sc0 += py;
-        sc1 += rr;
-      }
-    } else if constexpr (EPI == EPI_HVP) {
-      double uv[CPL];
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        const int c = lane + 32 * h;
-        uv[h] = (c < p) ? a.U[(size_t)j * a.ldu + c] : 0.0;
-      }
-      double acc2[CPL];
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) acc2[h] = 0.0;
-      const double *ks = gs + p * p;
-      for (int k = 0; k < p; ++k) {
-        const double yk = __shfl_sync(0xffffffffu, yv[k >> 5], k & 31);
-        const double uk = __shfl_sync(0xffffffffu, uv[k >> 5], k & 31);
-#pragma unroll
-        for (int h = 0; h < CPL; ++h) {
-          const int c = lane + 32 * h;
-          if (c < p) acc2[h] = fma(yk, ks[k * p + c], fma(uk, gs[k * p + c], acc2[h]));
-        }
-      }
-      double eh[CPL], ehy = 0.0;
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        eh[h] = 4.0 * (acc2[h] - pv[h]);
-        ehy += eh[h] * yv[h];
-      }
-      ehy = warp_sum(ehy);
-      const double rho = a.rho[j];
-      double uh = 0.0;
-#pragma unroll
-      for (int h = 0; h < CPL; ++h) {
-        const int c = lane + 32 * h;
-        const double hv = eh[h] - ehy * yv[h] - rho * uv[h];
-        uh += uv[h] * hv;
-        if (c < p) a.out[(size_t)j * a.ldo + c] = hv;
-      }
-      uh = warp_sum(uh);
-      if (lane == 0) sc0 += uh;
-    }
-  }
-  if constexpr (EPI == EPI_RAW) return;
-  double v[2] = {sc0, sc1};
-  __syncthreads();
-  block_sum<2>(v, scratch);
-  if (threadIdx.x == 0) {
-    a.tile_scal[2 * tile] = v[0];
-    a.tile_scal[2 * tile + 1] = v[1];
-    __threadfence();
-    s_ticket = atomicAdd(a.glob_cnt, 1u);
-  }
-  __syncthreads();
-  if (s_ticket != gridDim.x - 1) return;
-  __threadfence();
-  // tile scalars: thread t sums tiles t, t + blockDim, ... then a fixed-order block reduction
-  double tv[2] = {0.0, 0.0};
-  for (int t = threadIdx.x; t < (int)gridDim.x; t += blockDim.x) {
-    tv[0] += __ldcg(a.tile_scal + 2 * t);
-    tv[1] += __ldcg(a.tile_scal + 2 * t + 1);
-  }
-  block_sum<2>(tv, scratch);
-  if (threadIdx.x == 0) {
-    const double t0 = tv[0], t1 = tv[1];
-    if (a.scal_out) {
-      a.scal_out[0] = t0;
-      a.scal_out[1] = t1;
-    }
-    if constexpr (EPI == EPI_COSTGRAD) {
-      if (a.cost_out) a.cost_out[0] = a.gg[0] - 2.0 * t0 + a.cost_extra[0] + a.cost_extra[1];
-    }
-    *a.glob_cnt = 0u;
-  }
+  tile_epilogue<PT, EPI, BM, NTHREADS>(a, ptile, gs, scratch, &s_ticket, tile, j0, c0, n, p);
 }
 
 // V^T (pt_total x ldvt, row c = column c of V) from V (k x p, pitch ldv); rows >= p are not
@@ -379,6 +239,13 @@ __global__ void __launch_bounds__(256) transpose_kernel(int k, int p, const doub
     const int c = c0 + rr, i = i0 + tx;
     if (c < p && i < k) Vt[(size_t)c * ldvt + i] = t[tx][rr];
   }
+}
+
+cudaError_t symv_transpose(int k, int p, const double *V, int ldv, double *Vt, int64_t ldvt, const int *skip,
+                           cudaStream_t st) {
+  dim3 tg((k + 31) / 32, (p + 31) / 32);
+  transpose_kernel<<<tg, 256, 0, st>>>(k, p, V, ldv, Vt, ldvt, skip);
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------------------------------

@@ -98,6 +98,16 @@ def test_fixed_eval_large_p(ctx, n, p):
     check_fixed(g2, o, M, Y)
 
 
+@pytest.mark.parametrize("n,p", [(4100, 5), (5000, 16), (4096, 8), (4500, 1)])
+def test_fixed_eval_upper_triangle_path(ctx, n, p):
+    """n >= 4096, p <= 8: the upper-triangle product (symv_symm.cu: partial + reduce kernels),
+    including ragged n (not a multiple of the 128-row tile) and ragged p."""
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    g = gpu_fixed(ctx, M, Y, U)
+    check_fixed(g, sp.fixed_eval(M, Y, U), M, Y)
+
+
 @pytest.mark.parametrize("n,p", [(333, 16), (129, 5)])
 def test_fixed_eval_padded_pitch_and_split_calls(ctx, n, p):
     """ldm > n with NaN padding (must never be read) and HVP in a separate call."""

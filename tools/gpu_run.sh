@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-bash tools/gpu_profile.sh
-run() { tag=$1; d=$2; tl=$3; p0=$4; shift 4; timeout $((tl+90)) python tools/solve_run.py $d $tl $p0 "$@" > gpurun_out/exp_$tag.log 2> gpurun_out/exp_$tag.err; echo "$tag d=$d p0=$p0 $*: $(grep '"d"' gpurun_out/exp_$tag.log | cut -c1-200)"; }
-run T1 40 120 4 max_tcg=100
-run T2 40 120 4 max_tcg=300
-run T3 40 120 4 max_tcg=1000
+timeout 600 python -m pytest tests -m gpu -x -q -k "fixed_eval" > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+timeout 200 python tools/quick_sweep.py 16384,32768 8,16 > gpurun_out/sweep_symm.log 2>&1; cut -c1-140 gpurun_out/sweep_symm.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:symm -c 20 --csv --log-file gpurun_out/launch_symm.csv python tools/quick_sweep.py 32768 16 > /dev/null 2>&1; python tools/ncu_summary.py launches gpurun_out/launch_symm.csv | head -5
