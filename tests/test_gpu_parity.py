@@ -377,3 +377,22 @@ def test_solve_deterministic(ctx):
     strip = lambda tr: [{k: v for k, v in r.items() if k != "time_s"} for r in tr]
     assert strip(a[2]) == strip(b[2])
     assert np.array_equal(a[1]["Y"], b[1]["Y"])
+
+
+def test_solve_d40_against_stored_oracle(ctx):
+    """BASELINE configs[1] (d = 40, n = 821): GPU solve to eta_max <= 1e-8 (recomputed by the
+    oracle from the returned tuple) and objective within 1e-6 of the oracle's own full solve
+    (tests/golden/oracle_solves.json, written by tools/oracle_reference_solves.py from oracle/)."""
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_solves.json")))
+    ref = next(r for r in gold["solves"] if r["d"] == 40 and r["seed"] == 0)
+    Q, c = bqp_instance(40, 0)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 4, 0)
+    assert info["status"] == 0, info
+    assert abs(info["dual_obj"] - ref["dual_obj"]) <= 1e-6 * (1 + abs(ref["dual_obj"]))
+    amap, cnt, b = bqp.relax(Q, c)
+    X = ctx.solution(want_X=True)["X"]
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8, res["eta_max"]
