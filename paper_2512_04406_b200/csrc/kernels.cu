@@ -5,8 +5,10 @@
 //              deterministic CSR segmented sum over the index map (north star (d))
 //  assemble    M = A*(y) - C - T/sigma, with ||C + T/sigma||^2 (north star (a))
 //  dual_update T <- T - sigma (A*(y) - Y Y^T - C), ||R||, ||T||^2, <C,T>  (Alg. 2 step 6)
-//  vector ops  tangent projection (Lemma 4.1), row-normalisation retraction, the tCG
-//              updates with fused inner products, escape padding (Thm 4.5), Y W.
+//  vector ops  row-normalisation retraction, the tCG new direction (tangent projection,
+//              Lemma 4.1), fused inner products, escape padding (Thm 4.5)
+//  row epilogues for p > 64 (cost/gradient, HVP, z), A*(w) assembly for the TMA gather-product
+//  device tCG  Steihaug-Toint recurrences in device memory (tcg_init / tcg_update / tcg_newdir)
 // All reductions are fixed-order (block partials + last-block sum): results are bit-identical
 // from run to run.
 #include "common.cuh"
@@ -422,26 +424,6 @@ __global__ void __launch_bounds__(256) dot3_kernel(int n, int p, int ld, const d
   grid_sum<3>(v, part, counter, out, scratch);
 }
 
-// out = V - rowdot(V, Y) Y ;  optional scalar <out, out>
-__global__ void __launch_bounds__(256) project_kernel(int n, int p, int ld, const double *Y, const double *V,
-                                                      double *out, double *part, unsigned *counter,
-                                                      double *dots) {
-  __shared__ double scratch[8];
-  double v[1] = {0.0};
-  ROW_LOOP_BEGIN
-  const size_t o = (size_t)row * ld;
-  double d = 0.0;
-  for (int c = lane; c < p; c += 32) d = fma(V[o + c], Y[o + c], d);
-  d = warp_sum(d);
-  for (int c = lane; c < p; c += 32) {
-    const double x = V[o + c] - d * Y[o + c];
-    out[o + c] = x;
-    v[0] = fma(x, x, v[0]);
-  }
-  ROW_LOOP_END
-  if (dots) grid_sum<1>(v, part, counter, dots, scratch);
-}
-
 // out_row = (Y_row + t V_row) / ||Y_row + t V_row||; flag[0] = 1 if a norm <= 1e-14
 __global__ void __launch_bounds__(256) retract_kernel(int n, int p, int ld, const double *Y, const double *V,
                                                       double t, double *out, int *flag) {
@@ -461,37 +443,6 @@ __global__ void __launch_bounds__(256) retract_kernel(int n, int p, int ld, cons
     for (int c = lane; c < p; c += 32) out[o + c] = fma(t, V[o + c], Y[o + c]) * inv;
   }
   ROW_LOOP_END
-}
-
-// tCG step: eo = e + a d ; ho = h + a hd ; ro = r + a hd (ro optional)
-// dots = [<eo, g>, <eo, ho>, <ro, ro>, <eo, eo>]
-__global__ void __launch_bounds__(256) tcg_step_kernel(int n, int p, int ld, double alpha, const double *e,
-                                                       const double *d, double *eo, const double *h,
-                                                       const double *hd, double *ho, const double *r, double *ro,
-                                                       const double *g, double *part, unsigned *counter,
-                                                       double *dots) {
-  __shared__ double scratch[4 * 8];
-  double v[4] = {0.0, 0.0, 0.0, 0.0};
-  ROW_LOOP_BEGIN
-  const size_t o = (size_t)row * ld;
-  for (int c = lane; c < p; c += 32) {
-    const size_t k = o + c;
-    const double hdv = hd[k];
-    const double ev = fma(alpha, d[k], e[k]);
-    const double hv = fma(alpha, hdv, h[k]);
-    eo[k] = ev;
-    ho[k] = hv;
-    v[0] = fma(ev, g[k], v[0]);
-    v[1] = fma(ev, hv, v[1]);
-    v[3] = fma(ev, ev, v[3]);
-    if (ro) {
-      const double rv = fma(alpha, hdv, r[k]);
-      ro[k] = rv;
-      v[2] = fma(rv, rv, v[2]);
-    }
-  }
-  ROW_LOOP_END
-  grid_sum<4>(v, part, counter, dots, scratch);
 }
 
 // tCG new direction: d = P_Y(-r + beta d) in place; dots = [<d,d>]
@@ -530,33 +481,6 @@ __global__ void __launch_bounds__(256) repack_kernel(int n, int p_in, int ldi, c
     if (Vcols && c >= vcol0 && c < vcol0 + dv) x = Vcols[(size_t)(c - vcol0) * ldv_col + row];
     if (c >= p_out) x = 0.0;
     out[(size_t)row * ldo + c] = x;
-  }
-  ROW_LOOP_END
-}
-
-// out = normalize_rows(Y W), W p x r (row-major), out pitch ldo (columns >= r zeroed)
-__global__ void __launch_bounds__(256) apply_w_kernel(int n, int p, int ld, const double *Y, const double *W,
-                                                      int r, int ldo, double *out) {
-  ROW_LOOP_BEGIN
-  const size_t o = (size_t)row * ld;
-  double vals[8];
-  double s = 0.0;
-  // r <= 256 supported: lanes own columns lane + 32 h
-#pragma unroll
-  for (int h = 0; h < 8; ++h) {
-    const int c = lane + 32 * h;
-    double x = 0.0;
-    if (c < r)
-      for (int k = 0; k < p; ++k) x = fma(Y[o + k], W[k * r + c], x);
-    vals[h] = x;
-    s = fma(x, x, s);
-  }
-  s = warp_sum(s);
-  const double inv = 1.0 / sqrt(s);
-#pragma unroll
-  for (int h = 0; h < 8; ++h) {
-    const int c = lane + 32 * h;
-    if (c < ldo) out[(size_t)row * ldo + c] = (c < r) ? vals[h] * inv : 0.0;
   }
   ROW_LOOP_END
 }
@@ -878,21 +802,9 @@ cudaError_t dot3_launch(int n, int p, int ld, const double *A0, const double *B0
   dot3_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, A0, B0, A1, B1, A2, B2, part, counter, out);
   return cudaGetLastError();
 }
-cudaError_t project_launch(int n, int p, int ld, const double *Y, const double *V, double *out, double *part,
-                           unsigned *counter, double *dots, cudaStream_t st) {
-  project_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, V, out, part, counter, dots);
-  return cudaGetLastError();
-}
 cudaError_t retract_launch(int n, int p, int ld, const double *Y, const double *V, double t, double *out,
                            int *flag, cudaStream_t st) {
   retract_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, V, t, out, flag);
-  return cudaGetLastError();
-}
-cudaError_t tcg_step_launch(int n, int p, int ld, double alpha, const double *e, const double *d, double *eo,
-                            const double *h, const double *hd, double *ho, const double *r, double *ro,
-                            const double *g, double *part, unsigned *counter, double *dots, cudaStream_t st) {
-  tcg_step_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, alpha, e, d, eo, h, hd, ho, r, ro, g, part, counter,
-                                                dots);
   return cudaGetLastError();
 }
 cudaError_t newdir_launch(int n, int p, int ld, const double *Y, const double *r, double beta, double *d,
@@ -903,12 +815,6 @@ cudaError_t newdir_launch(int n, int p, int ld, const double *Y, const double *r
 cudaError_t repack_launch(int n, int p_in, int ldi, const double *in, int p_out, int ldo, double *out, int vcol0,
                           int dv, const double *Vcols, int64_t ldv_col, cudaStream_t st) {
   repack_kernel<<<rows_grid(n), 256, 0, st>>>(n, p_in, ldi, in, p_out, ldo, out, vcol0, dv, Vcols, ldv_col);
-  return cudaGetLastError();
-}
-cudaError_t apply_w_launch(int n, int p, int ld, const double *Y, const double *W, int r, int ldo, double *out,
-                           cudaStream_t st) {
-  if (r > 256) return cudaErrorInvalidValue;
-  apply_w_kernel<<<rows_grid(n), 256, 0, st>>>(n, p, ld, Y, W, r, ldo, out);
   return cudaGetLastError();
 }
 cudaError_t make_x_launch(int n, const double *T, int64_t ldt, const double *z, double *X, cudaStream_t st) {

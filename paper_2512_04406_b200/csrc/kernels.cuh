@@ -91,19 +91,12 @@ inline int dual_update_blocks(int n) { return ((n + 31) / 32) * ((n + 31) / 32);
 cudaError_t dot3_launch(int n, int p, int ld, const double *A0, const double *B0, const double *A1,
                         const double *B1, const double *A2, const double *B2, double *part, unsigned *counter,
                         double *out, cudaStream_t st);
-cudaError_t project_launch(int n, int p, int ld, const double *Y, const double *V, double *out, double *part,
-                           unsigned *counter, double *dots, cudaStream_t st);
 cudaError_t retract_launch(int n, int p, int ld, const double *Y, const double *V, double t, double *out,
                            int *flag, cudaStream_t st);
-cudaError_t tcg_step_launch(int n, int p, int ld, double alpha, const double *e, const double *d, double *eo,
-                            const double *h, const double *hd, double *ho, const double *r, double *ro,
-                            const double *g, double *part, unsigned *counter, double *dots, cudaStream_t st);
 cudaError_t newdir_launch(int n, int p, int ld, const double *Y, const double *r, double beta, double *d,
                           double *part, unsigned *counter, double *dots, cudaStream_t st);
 cudaError_t repack_launch(int n, int p_in, int ldi, const double *in, int p_out, int ldo, double *out, int vcol0,
                           int dv, const double *Vcols, int64_t ldv_col, cudaStream_t st);
-cudaError_t apply_w_launch(int n, int p, int ld, const double *Y, const double *W, int r, int ldo, double *out,
-                           cudaStream_t st);
 cudaError_t make_x_launch(int n, const double *T, int64_t ldt, const double *z, double *X, cudaStream_t st);
 cudaError_t vdot_launch(int64_t len, const double *a, const double *b, double *part, unsigned *counter,
                         double *out, cudaStream_t st);

@@ -108,6 +108,37 @@ def test_fixed_eval_upper_triangle_path(ctx, n, p):
     check_fixed(g, sp.fixed_eval(M, Y, U), M, Y)
 
 
+@pytest.mark.parametrize("n,p", [(1, 1), (2, 3), (5, 64), (64, 1024), (300, 1024)])
+def test_fixed_eval_degenerate_and_max_p(ctx, n, p):
+    """Degenerate sizes (n = 1, p > n) and the largest factor width DRSDP_MAX_P = 1024."""
+    M = sweep_matrix_cpu(n) if n > 1 else np.array([[0.7]])
+    Y, U = sweep_factor(n, p)
+    g = gpu_fixed(ctx, M, Y, U)
+    check_fixed(g, sp.fixed_eval(M, Y, U), M, Y)
+
+
+def test_abi_argument_and_state_errors(ctx):
+    from paper_2512_04406_b200 import abi
+
+    n = 40
+    M = dev(sweep_matrix_cpu(n))
+    ctx.set_subproblem_matrix(n, M, n)
+    Y, U = sweep_factor(n, 4)
+    Yd, Ud = dev(Y), dev(U)
+    H = torch.empty_like(Yd)
+    for bad_p in (0, 1025):
+        with pytest.raises(abi.DrsdpError) as e:
+            ctx.subproblem_eval(abi.EVAL_COSTGRAD, bad_p, Yd, None, None, None, H, None)
+        assert e.value.code == abi.ERR_INVALID_ARG
+    Y2 = dev(Y.copy())
+    with pytest.raises(abi.DrsdpError) as e:  # HVP at a Y without a prior COSTGRAD there
+        ctx.subproblem_eval(abi.EVAL_HVP, 4, Y2, Ud, None, None, None, H)
+    assert e.value.code == abi.ERR_STATE
+    with pytest.raises(abi.DrsdpError) as e:  # HVP without U
+        ctx.subproblem_eval(abi.EVAL_COSTGRAD | abi.EVAL_HVP, 4, Yd, None, None, None, H, H)
+    assert e.value.code == abi.ERR_INVALID_ARG
+
+
 @pytest.mark.parametrize("n,p", [(333, 16), (129, 5)])
 def test_fixed_eval_padded_pitch_and_split_calls(ctx, n, p):
     """ldm > n with NaN padding (must never be read) and HVP in a separate call."""
