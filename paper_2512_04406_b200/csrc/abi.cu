@@ -75,7 +75,7 @@ int choose_splits(drsdp_ctx *ctx, int krows, int ntiles) {
 int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
   (void)n;
   (void)p;
-  CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64), "alloc gram workspace");
+  CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64 + 64), "alloc gram workspace");
   return DRSDP_OK;
 }
 

@@ -22,7 +22,7 @@ namespace drsdp {
 __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *__restrict__ Y, int ldy,
                                                    const double *__restrict__ U, int ldu, int rows_per_block,
                                                    double *part, unsigned *counter, double *G, double *K,
-                                                   double *gg, const int *skip) {
+                                                   double *gg, const int *skip, int split_final) {
   if (skip && *(volatile const int *)skip) return;
   extern __shared__ double sh[];
   const int pp = p * p;
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *_
     const int e = threadIdx.x + k * 256;
     if (e < nval) mine[e] = acc[k];
   }
+  if (split_final) return;  // gram_final_kernel sums the partials
   __threadfence();
   __syncthreads();
   __shared__ unsigned ticket;
@@ -92,6 +93,27 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *_
   }
 }
 
+// second phase for large p x p results: thread e sums entry e over the nb block partials (in block
+// order), G / K written, ||G||^2 by a deterministic grid reduction
+__global__ void __launch_bounds__(256) gram_final_kernel(int nval, int pp, int nb, const double *__restrict__ part,
+                                                         double *G, double *K, double *gg, double *red,
+                                                         unsigned *counter, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
+  __shared__ double scratch[8];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  double v[1] = {0.0};
+  if (e < nval) {
+    const double s = ordered_sum(part + e, nb, (size_t)nval);
+    if (e < pp) {
+      G[e] = s;
+      v[0] = s * s;
+    } else {
+      K[e - pp] = s;
+    }
+  }
+  grid_sum<1>(v, red, counter, gg, scratch);
+}
+
 cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
   const int nval = a.U ? 2 * a.p * a.p : a.p * a.p;
   if (nval > 32 * 256) return cudaErrorInvalidValue;
@@ -101,8 +123,16 @@ cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
   int rpb = (a.n + nb - 1) / nb;
   nb = (a.n + rpb - 1) / rpb;
   const size_t smem = (size_t)2 * 32 * a.p * 8;
+  // large results: the single last block would sum nb x nval partials serially (~10 us per entry
+  // at nb = 296); a second kernel spreads that over nval threads
+  const int split_final = nval > 1024 ? 1 : 0;
   gram_kernel<<<nb, 256, smem, st>>>(a.n, a.p, a.Y, a.ldy, a.U, a.ldu, rpb, a.part, a.counter, a.G, a.K, a.gg,
-                                     a.skip);
+                                     a.skip, split_final);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !split_final) return e;
+  double *red = a.part + (size_t)nb * nval;
+  gram_final_kernel<<<(nval + 255) / 256, 256, 0, st>>>(nval, a.p * a.p, nb, a.part, a.G, a.K, a.gg, red, a.counter,
+                                                        a.skip);
   return cudaGetLastError();
 }
 
