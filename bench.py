@@ -426,7 +426,11 @@ def run_gpu(args):
             t0 = time.perf_counter()
             info = ctx.solve()
             wall = time.perf_counter() - t0
-            solves.append({"d": d, "n": nn, "seconds": wall, "status": "converged" if info["status"] == 0 else
+            paper = {10: 0.07, 20: 0.24, 30: 1.44, 40: 2.69, 50: 15.0, 60: 115.0, 70: 227.0, 80: 776.0}.get(d)
+            solves.append({"d": d, "n": nn, "seconds": wall, "paper_mean_seconds": paper,
+                           "paper_context": "ManiDSDP, MATLAB on an i9-10900 CPU, N(0,1) instances (P:789-798); "
+                                            "context only, not the same instances",
+                           "status": "converged" if info["status"] == 0 else
                            "not_converged", "outer_iters": info["outer_iters"], "p_max": info["p_max"],
                            "eta_p": info["eta_p"], "eta_d": info["eta_d"], "eta_g": info["eta_g"],
                            "dual_obj": info["dual_obj"], "n_costgrad": info["n_costgrad"], "n_hvp": info["n_hvp"]})
