@@ -263,10 +263,15 @@ struct Run {
 
   // Riemannian trust region (oracle/rtr.py rtr); s->cur holds Y on entry, the result on exit.
   bool debug = std::getenv("DRSDP_DEBUG_RTR") != nullptr;
+  // diagnostics of the last inner solve (DRSDP_VERBOSE)
+  int last_exit = 0;  // 0 gradient tolerance, 1 stagnation, 2 max_rtr, 3 tiny radius
+  double last_warm_t = -1.0, last_gn0 = 0.0;
   int rtr(int p, double grad_tol, bool warm, int &iters_out, int &tcg_out) {
     RC(costgrad_at(s->cur, p));
+    last_warm_t = -1.0;
     if (warm) {
       double t = 1.0;
+      last_warm_t = 0.0;
       for (int h = 0; h < 25; ++h) {
         bool bad = false;
         RC(retract_into(s->cur.Y, s->Uw.ptr, t, s->prop.Y, p, bad));
@@ -274,12 +279,15 @@ struct Run {
           RC(costgrad_at(s->prop, p));
           if (s->prop.f < s->cur.f) {
             swap_pts();
+            last_warm_t = t;
             break;
           }
         }
         t *= 0.5;
       }
     }
+    last_gn0 = s->cur.gn;
+    last_exit = 2;
     const double delta_bar = std::sqrt((double)n);
     double Delta = delta_bar / 8.0;
     const int max_tcg = prm.max_tcg > 0 ? prm.max_tcg : std::max(1, n * (p - 1));
@@ -290,11 +298,15 @@ struct Run {
     double best_gn = s->cur.gn;
     int since_best = 0;
     for (int it = 0; it < prm.max_rtr; ++it) {
-      if (s->cur.gn <= grad_tol) break;
+      if (s->cur.gn <= grad_tol) {
+        last_exit = 0;
+        break;
+      }
       if (s->cur.gn <= 0.5 * best_gn) {
         best_gn = s->cur.gn;
         since_best = 0;
       } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr) {
+        last_exit = 1;
         break;
       }
       ++iters_out;
@@ -342,8 +354,12 @@ struct Run {
       else if (rho > 0.75 && hit)
         Delta = std::min(2.0 * Delta, delta_bar);
       if (rhoden >= 0 && rho > 0.1) swap_pts();
-      if (Delta < 1e-300) break;
+      if (Delta < 1e-300) {
+        last_exit = 3;
+        break;
+      }
     }
+    if (iters_out == 0 && s->cur.gn <= grad_tol) last_exit = 0;
     return DRSDP_OK;
   }
 };
@@ -643,9 +659,17 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     const double eta_max = std::max(eta_p, std::max(eta_d, eta_g));
     double row[13] = {(double)(k + 1), eta_p, eta_d, eta_g, eta_max, pobj, dobj, run.sigma, (double)p,
                       (double)rtr_it, (double)tcg_it, 0.0, 0.0};
-    if (verbose)
-      std::fprintf(stderr, "[drsdp] k=%d p=%d sigma=%.3e eta_p=%.3e eta_d=%.3e eta_g=%.3e dobj=%.12f rtr=%d tcg=%d t=%.2fs\n",
-                   k + 1, p, run.sigma, eta_p, eta_d, eta_g, dobj, rtr_it, tcg_it, now_s() - t0);
+    if (verbose) {
+      int nneg = 0;
+      const double th = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
+      while (nneg < n && lam[nneg] < th) ++nneg;
+      std::fprintf(stderr,
+                   "[drsdp] k=%d p=%d sigma=%.3e eta_p=%.3e eta_d=%.3e eta_g=%.3e dobj=%.12f rtr=%d tcg=%d exit=%s "
+                   "gn0=%.2e gn=%.2e tol=%.2e warm_t=%.2g neg=%d lmin=%.3e lmax=%.3e t=%.2fs\n",
+                   k + 1, p, run.sigma, eta_p, eta_d, eta_g, dobj, rtr_it, tcg_it,
+                   run.last_exit == 0 ? "tol" : run.last_exit == 1 ? "stall" : run.last_exit == 2 ? "maxit" : "radius",
+                   run.last_gn0, s->cur.gn, grad_tol, run.last_warm_t, nneg, lam[0], lam[n - 1], now_s() - t0);
+    }
     if (eta_max <= prm.tol) {
       status = DRSDP_OK;
       row[12] = now_s() - t0;

@@ -427,3 +427,29 @@ def test_solve_d40_against_stored_oracle(ctx):
     X = ctx.solution(want_X=True)["X"]
     res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
     assert res["eta_max"] <= 1e-8, res["eta_max"]
+
+
+def test_solve_general_problem_with_cost_matrix(ctx):
+    """(DSDP) with C != 0 through drsdp_set_problem (COO map, host C): exercises A(C), the
+    C terms of the ALM cost / assembly / dual update, eta_p's 1 + ||C|| and pobj = <C, T> + 1^T z
+    (reading R7) against the oracle's solve of the same problem."""
+    from inputs import random_symmetric
+
+    Q, c = bqp_instance(5, 3)
+    amap, cnt, b = bqp.relax(Q, c)
+    n, m = amap.shape[0], cnt.size
+    C = 0.3 * random_symmetric(n, 11)
+    np.fill_diagonal(C, 0.0)
+    iu, ju = np.triu_indices(n)
+    ctx.set_problem(n, m, C, iu, ju, amap[iu, ju], b)
+    ctx.set_params(ctx.default_params(p0=2))
+    ctx.set_initial_factor(initial_factor(n, 2, 0))
+    info = ctx.solve()
+    assert info["status"] == 0, info
+    o = admm.solve(amap, cnt, b, C, admm.Params(p0=2), initial_factor(n, 2, 0))
+    assert o["status"] == "converged"
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+    sol = ctx.solution(want_X=True)
+    res = admm.residues(amap, cnt, b, C, sol["y"], sol["Y"], sol["X"] + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8
+    assert abs(res["primal_obj"] - info["primal_obj"]) <= 1e-8 * (1 + abs(res["primal_obj"]))
