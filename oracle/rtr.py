@@ -102,12 +102,13 @@ def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, 
     for it in range(prm.max_iter):
         if gn <= grad_tol:
             break
-        # stagnation exit (reading R30): ||grad|| has not halved within `stall` iterations
+        # stagnation exit (reading R30): ||grad|| has not halved within `stall`
+        # iterations and is within 100x of the tolerance
         if gn <= 0.5 * best_gn:
             best_gn, since_best = gn, 0
         else:
             since_best += 1
-            if stall > 0 and since_best > stall:
+            if stall > 0 and since_best > stall and gn <= 100.0 * grad_tol:
                 break
         info["iters"] += 1
         eta, Heta, nin, hit = tcg(prob, ctx, Y, g, Delta, prm)
