@@ -61,7 +61,7 @@ struct SolverState {
   struct Graph {
     const double *Y = nullptr;
     int p = -1, ldp = -1;
-    bool warm = false;
+    bool warm = false, failed = false;  // failed: graph capture unsupported, use batched launches
     cudaGraphExec_t exec = nullptr;
   } graphs[2];
   cudaStream_t priv = nullptr;   // private capture-capable stream used for the whole solve
@@ -167,35 +167,47 @@ struct Run {
     return DRSDP_OK;
   }
 
+  // Returns DRSDP_OK with g.exec set, or DRSDP_OK with g.exec == nullptr when the graph could not
+  // be built (the caller then keeps the batched launches); kernel-launch errors inside the body
+  // are real errors and are returned.
   int capture_graph(SolverState::Graph &g, int p) {
     cudaGraph_t graph = nullptr, body_out = nullptr;
-    CK(cudaGraphCreate(&graph, 0), "graph create");
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    auto give_up = [&](cudaGraph_t gr) {
+      if (gr) cudaGraphDestroy(gr);
+      cudaGetLastError();
+      g.failed = true;
+      return DRSDP_OK;
+    };
+    if (cudaGraphCreate(&graph, 0) != cudaSuccess) return give_up(nullptr);
     cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault), "conditional handle");
+    if (cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) return give_up(graph);
     cudaGraphNodeParams cp = {};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = h;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp), "conditional node");
-    CK(cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                     cudaStreamCaptureModeRelaxed),
-       "begin capture");
+    if (cudaGraphAddNode(&node, graph, nullptr, 0, &cp) != cudaSuccess) return give_up(graph);
+    if (cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed) != cudaSuccess)
+      return give_up(graph);
     ctx->skip_flag = &s->tcg.ptr->done;
     int rc = tcg_body(p, h, 1);
     ctx->skip_flag = nullptr;
-    cudaError_t e = cudaStreamEndCapture(ctx->stream, &body_out);
+    const cudaError_t e = cudaStreamEndCapture(ctx->stream, &body_out);
     if (rc) {
       cudaGraphDestroy(graph);
       return rc;
     }
-    CK(e, "end capture");
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g.exec = nullptr;
-    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    if (e != cudaSuccess) return give_up(graph);
+    const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
-    CK(e, "graph instantiate");
+    if (ei != cudaSuccess) {
+      g.exec = nullptr;
+      return give_up(nullptr);
+    }
     return DRSDP_OK;
   }
 
@@ -221,7 +233,7 @@ struct Run {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       g.exec = nullptr;
     }
-    if (graphs_ok && g.warm && !g.exec) RC(capture_graph(g, p));
+    if (graphs_ok && g.warm && !g.exec && !g.failed) RC(capture_graph(g, p));
     if (graphs_ok && g.exec) {
       CK(cudaGraphLaunch(g.exec, ctx->stream), "graph launch");
       ctx->launches += 1;
