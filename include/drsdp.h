@@ -122,7 +122,8 @@ typedef struct {
   uint64_t seed;                       /* Y^0 draw when no initial factor is given                */
   double rho_reg;                      /* trust-region ratio regularisation: max(1,|f|) eps rho_reg (R12) */
   int32_t stall_rtr;                   /* stagnation: stop RTR when ||grad|| has not halved within
-                                          stall_rtr iterations (0 = never; reading R30)            */
+                                          stall_rtr iterations and is within 100x of the inner
+                                          tolerance (0 = never; reading R30)                       */
   int32_t reserved;
 } drsdp_params;
 
@@ -146,7 +147,10 @@ typedef struct {
   double seconds;                        /* wall time of drsdp_solve                             */
 } drsdp_info;
 
-/* Runs Algorithm 2 to eta_max <= tol. Returns OK or ERR_NOT_CONVERGED (info filled either way). */
+/* Runs Algorithm 2 to eta_max <= tol. Returns OK or ERR_NOT_CONVERGED (info filled either way).
+ * Synchronous: it orders itself after the work already queued on the context stream, runs on a
+ * private stream (the inner truncated CG is a captured CUDA graph), and returns when done.
+ * Environment: DRSDP_VERBOSE=1 prints one diagnostic line per outer iteration to stderr. */
 int drsdp_solve(drsdp_ctx *ctx, drsdp_info *info);
 
 /* Final tuple: y (m), the factor Y of S = YY^T (n*p_final; pass NULL to skip), p_final,
