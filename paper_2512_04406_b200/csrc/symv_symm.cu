@@ -18,6 +18,8 @@
 // p = 16, +12.5 % at p = 8).
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "symv.cuh"
 #include "tile_epilogue.cuh"
@@ -65,7 +67,7 @@ template <int PT>
 struct SCfg {
   static constexpr int CB = PT / 8;              // column fragments
   static constexpr int WM = BM / NCW, JB = WM / 8;  // forward warp tile 16 x PT
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = PT >= 16 ? 2 : 3;  // PT = 16: 2 CTAs per SM (88 KB each)
   static constexpr int A_ELEMS = BM * BK, V_ELEMS = PT * BK;
   static constexpr int STAGE_ELEMS = A_ELEMS + V_ELEMS;
   static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
@@ -78,7 +80,7 @@ struct SCfg {
 }  // namespace
 
 template <int PT>
-__global__ void __launch_bounds__(NTA, 1)
+__global__ void __launch_bounds__(NTA, PT >= 16 ? 2 : 1)
     symm_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
                         const int4 *__restrict__ units, double *__restrict__ Fpart, double *__restrict__ Tpart,
                         const int *skip) {
@@ -322,7 +324,8 @@ static cudaError_t symm_t(const SymvArgs &a, int epi, const CUtensorMap &mA, con
 bool symm_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
   // p <= 8: measured on B200 (n = 32768) 0.97 ms vs 1.31 ms for the full-matrix kernel; at p = 16 the
   // doubled DMMA work per byte makes this variant DMMA/shared-memory bound (1.69 ms vs 1.37 ms)
-  return mode2 == MODE2_NONE && !atr && (a.k == 0 || a.k == a.n) && a.p <= 8 && a.A2 == nullptr &&
+  static const bool p16 = std::getenv("DRSDP_SYMM16") != nullptr;  // experiment: p <= 16
+  return mode2 == MODE2_NONE && !atr && (a.k == 0 || a.k == a.n) && a.p <= (p16 ? 16 : 8) && a.A2 == nullptr &&
          !(a.lda & 1) && !((uintptr_t)a.A & 15) && encoder() != nullptr && (epi != EPI_RAW || a.p <= 16);
 }
 
