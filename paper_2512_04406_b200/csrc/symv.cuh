@@ -73,6 +73,7 @@ cudaError_t symv_launch(const SymvArgs &a, int epi, int mode2, bool atr, int S, 
 // into Vt (ceil(p/PT)*PT... rows p, pitch ldvt = even >= n) first.
 bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr);
 int symv_tma_rows();
+int symv_tma_ctas_per_sm(int p);
 int symv_tma_kstep();
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st);
 // Vt (p x ldvt) = V^T for a k x p row-major V (pitch ldv)

@@ -76,7 +76,10 @@ struct Cfg {
   static constexpr int WR = NCW / WC;           // warps across rows
   static constexpr int WM = BM / WR, WN = PT / WC;
   static constexpr int JB = WM / 8, CB = WN / 8;
-  static constexpr int STAGES = PT >= 64 ? 3 : 4;
+  // PT <= 16: 3 stages so that two CTAs share an SM (one streams while the other runs its epilogue);
+  // PT >= 32: one CTA per SM with a deeper ring
+  static constexpr int CTAS_PER_SM = PT <= 16 ? 2 : 1;
+  static constexpr int STAGES = PT >= 64 ? 3 : (PT <= 16 ? 3 : 4);
   static constexpr int A_ELEMS = BM * BK, V_ELEMS = PT * BK;
   static constexpr int STAGE_ELEMS = A_ELEMS + V_ELEMS;
   static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
@@ -94,7 +97,7 @@ struct Cfg {
 // [0, kpad) come from (tmA, tmV), those in [kpad, 2 kpad) from (tmA2, tmV2), kpad = n rounded up
 // to a multiple of BK (TMA zero-fills the padding columns).
 template <int PT, int EPI, bool PAIR>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
     symv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmV2, SymvArgs a) {
   using C = Cfg<PT>;
@@ -291,6 +294,7 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
 }
 
 int symv_tma_rows() { return BM; }
+int symv_tma_ctas_per_sm(int p) { return symv_pt(p) <= 16 ? 2 : 1; }
 int symv_tma_kstep() { return BK; }
 
 template <int PT, int EPI, bool PAIR>
