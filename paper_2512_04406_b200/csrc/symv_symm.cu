@@ -80,7 +80,7 @@ struct SCfg {
 }  // namespace
 
 template <int PT>
-__global__ void __launch_bounds__(NTA, PT >= 16 ? 2 : 1)
+__global__ void __launch_bounds__(NTA, 2)
     symm_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
                         const int4 *__restrict__ units, double *__restrict__ Fpart, double *__restrict__ Tpart,
                         const int *skip) {
