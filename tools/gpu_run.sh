@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 200 python tools/quick_sweep.py 4096,16384,32768 8 > gpurun_out/sweep.log 2>&1; cut -c1-110 gpurun_out/sweep.log
-timeout 600 python -m pytest tests -m gpu -x -q -k "upper_triangle" > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+bash tools/gpu_profile.sh
