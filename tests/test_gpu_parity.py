@@ -453,3 +453,23 @@ def test_solve_general_problem_with_cost_matrix(ctx):
     res = admm.residues(amap, cnt, b, C, sol["y"], sol["Y"], sol["X"] + np.diag(sol["z"]))
     assert res["eta_max"] <= 1e-8
     assert abs(res["primal_obj"] - info["primal_obj"]) <= 1e-8 * (1 + abs(res["primal_obj"]))
+
+
+def test_fixed_m_mode_first_iterations(ctx):
+    """mode = 1 (the north-star literal fixed-M ADMM step, reading R2's switch): the first outer
+    iteration from the same Y^0 reaches the same subproblem solution as the oracle's fixed mode
+    (dual objective and residues after one ADMM step), and later iterations stay finite."""
+    Q, c = bqp_instance(5, 1)
+    amap, cnt, b = bqp.relax(Q, c)
+    n = amap.shape[0]
+    ctx.set_bqp(Q, c)
+    ctx.set_params(ctx.default_params(p0=2, mode=1, max_outer=3))
+    ctx.set_initial_factor(initial_factor(n, 2, 1))
+    info = ctx.solve()
+    tr = ctx.trace()
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2, mode="fixed", max_outer=3), initial_factor(n, 2, 1))
+    assert len(tr) == 3 and all(np.isfinite(r["eta_max"]) for r in tr)
+    r0, q0 = tr[0], o["trace"][0]
+    assert abs(r0["dual_obj"] - q0["dual_obj"]) <= 1e-6 * (1 + abs(q0["dual_obj"]))
+    for k in ("eta_p", "eta_g"):
+        assert abs(r0[k] - q0[k]) <= 1e-6 * (1 + abs(q0[k])), k

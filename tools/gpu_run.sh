@@ -1,4 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-bash tools/gpu_profile.sh
+timeout 300 python -m pytest tests -m gpu -x -q -k "fixed_m_mode" > gpurun_out/pt.log 2>&1; tail -25 gpurun_out/pt.log | grep -E "assert|Error|passed|failed|where" | head -12
