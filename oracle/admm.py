@@ -188,8 +188,11 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
             trace.append(row)
             break
         Vs = escape_directions(res["lam"], res["V"], prm.eig_neg_tol, prm.escape_max)
-        # rank tolerance tied to the residual (reading R32)
-        Y = rank_reduce(Y, min(prm.rank_tol, max(1e-8, 0.01 * math.sqrt(res["eta_max"]))))
+        # rank tolerance tied to the residual (reading R32); no reduction in an iteration that
+        # escapes (reading R34: the escape columns of the previous iteration are O(sqrt(|lambda|/sigma))
+        # and a relative tolerance would remove them before they grow)
+        if Vs is None:
+            Y = rank_reduce(Y, min(prm.rank_tol, max(1e-8, 0.01 * math.sqrt(res["eta_max"]))))
         if Vs is not None:
             delta = Vs.shape[1]
             pr = Y.shape[1]

@@ -694,10 +694,12 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
     int dv = 0;
     while (dv < prm.escape_max && dv < n && lam[dv] < thresh) ++dv;
-    // rank reduction (readings R15, R32): compress Y to its numerical rank at the tolerance
-    // rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta_max))). Eigenpairs of the p x p
-    // Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so row/column-major agree).
-    {
+    if (dv > 0 && p + dv > std::min(DRSDP_MAX_P, n)) dv = std::max(0, std::min(DRSDP_MAX_P, n) - p);
+    // rank reduction (readings R15, R32, R34): only in an iteration that does not escape, compress
+    // Y to its numerical rank at the tolerance rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta_max))).
+    // Eigenpairs of the p x p Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so
+    // row/column-major agree).
+    if (dv == 0) {
       CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
          "copy G");
       const int lw = (int)s->gwork.cap - 1;
@@ -728,7 +730,6 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
         p = r;
       }
     }
-    if (dv > 0 && p + dv > std::min(DRSDP_MAX_P, n)) dv = std::max(0, std::min(DRSDP_MAX_P, n) - p);
     if (dv > 0) {
       if (p + dv > s->ldp) RC(set_pitch(ctx, ((p + dv + 63) / 64) * 64, true, p));
       // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]

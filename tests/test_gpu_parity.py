@@ -427,6 +427,35 @@ def test_solve_d40_against_stored_oracle(ctx):
     X = ctx.solution(want_X=True)["X"]
     res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
     assert res["eta_max"] <= 1e-8, res["eta_max"]
+    _check_p_update(tr)
+
+
+def _check_p_update(tr):
+    """Readings R15/R34: escape (p grows by exactly delta) xor rank reduction (p does not grow)."""
+    for r0, r1 in zip(tr, tr[1:]):
+        if r0["escape_delta"] > 0:
+            assert r1["p"] == r0["p"] + r0["escape_delta"], (r0, r1)
+        else:
+            assert r1["p"] <= r0["p"], (r0, r1)
+
+
+def test_solve_d70_converges(ctx):
+    """d = 70 (n = 2486, the paper's Table 1 size range): the solve reaches
+    eta_max <= 1e-8, recomputed by the oracle's residue formulas from the returned tuple, and
+    its value is a lower bound of the BQP (checked against the value of a rounded point).
+    This instance cycled at eta_d ~ 1e-5 before reading R34."""
+    Q, c = bqp_instance(70, 0)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 4, 0)
+    assert info["status"] == 0, info
+    amap, cnt, b = bqp.relax(Q, c)
+    X = ctx.solution(want_X=True)["X"]
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8, res["eta_max"]
+    assert abs(res["dual_obj"] - info["dual_obj"]) <= 1e-9 * (1 + abs(info["dual_obj"]))
+    Y = sol["Y"]
+    x = np.where(Y[1:71] @ Y[0] >= 0, 1.0, -1.0)
+    assert info["dual_obj"] <= bqp.bqp_value(Q, c, x) + 1e-6
+    _check_p_update(tr)
 
 
 def test_solve_general_problem_with_cost_matrix(ctx):

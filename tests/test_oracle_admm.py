@@ -115,6 +115,20 @@ def test_d10_solve_brute_force_and_invariants(seed):
     assert abs(out["y"][0] - 1.0) <= 1e-8
 
 
+def test_p_update_escape_xor_reduce():
+    """Readings R15/R34: an outer iteration either pads Y with its escape columns (p_{k+1} =
+    p_k + delta_k exactly) or, when X has no escape directions, compresses Y (p_{k+1} <= p_k)."""
+    for d, seed in ((10, 0), (12, 1)):
+        Q, c, amap, cnt, b, prm, Y0 = _solve(d, seed, p0=2)
+        tr = admm.solve(amap, cnt, b, None, prm, Y0)["trace"]
+        assert any(r["escape_delta"] > 0 for r in tr)
+        for r0, r1 in zip(tr, tr[1:]):
+            if r0["escape_delta"] > 0:
+                assert r1["p"] == r0["p"] + r0["escape_delta"]
+            else:
+                assert r1["p"] <= r0["p"]
+
+
 def test_residue_diving_behaviour():
     """Reported, not gated by the paper (Fig. 3, single instances): the last outer
     iteration drops log10 eta_max by >= 4 decades on at least one of 3 seeds (with the inexact

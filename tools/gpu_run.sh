@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests -m gpu -x -q -k "fixed_m_mode" > gpurun_out/pt.log 2>&1; tail -25 gpurun_out/pt.log | grep -E "assert|Error|passed|failed|where" | head -12
+for d in 100 80; do
+  DRSDP_VERBOSE=1 timeout 1300 python tools/solve_run.py $d 1200 > gpurun_out/solve_r34_$d.log 2> gpurun_out/solve_r34_${d}_v.log
+  tail -1 gpurun_out/solve_r34_$d.log | cut -c1-400
+done
