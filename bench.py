@@ -8,8 +8,8 @@ n = 32768 (M = 8.6 GB, far larger than the 126 MB L2: no flush needed), p = 16 b
 One step = one cost+gradient+Riemannian-gradient evaluation followed by one Hessian-vector
 product at the same Y (the "grad+HVP" pair of the metric), i.e. 2 subproblem evaluations.
 value = evaluations/s (whole job; 2 per step). The other sweep points (n in {4096, 16384, 32768} x
-p in {8, 16, 32, 64}) and full ManiDSDP solves of the dense BQPs d = 10 and d = 40 (configs[0..1],
-"solve time to KKT 1e-8") are reported in the same JSON line under "sweep" and "solves".
+p in {8, 16, 32, 64}) and full ManiDSDP solves of the dense BQPs d = 10, 40 (configs[0..1], "solve time to
+KKT 1e-8") and d = 80 (the paper's largest dense size) are reported in the same JSON line under "sweep" and "solves".
 
 Multi-GPU (--gpus N under torchrun): the subproblem does not shard in this round (DESIGN.md
 "replicas only"): every rank runs the same workload on its own GPU, no collective on the data
@@ -463,7 +463,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--solve-d", type=lambda s: [int(x) for x in s.split(",") if x], default=[10, 40])
+    ap.add_argument("--solve-d", type=lambda s: [int(x) for x in s.split(",") if x], default=[10, 40, 80])
     ap.add_argument("--solve-time-limit", type=float, default=120.0)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-budget", type=float, default=10.0)

@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-for d in 100 80; do
-  DRSDP_VERBOSE=1 timeout 1300 python tools/solve_run.py $d 1200 > gpurun_out/solve_r34_$d.log 2> gpurun_out/solve_r34_${d}_v.log
-  tail -1 gpurun_out/solve_r34_$d.log | cut -c1-400
+i=0
+for args in "escape_max=32" "mode=1" "escape_max=32 mode=1"; do
+  i=$((i+1))
+  DRSDP_VERBOSE=1 timeout 560 python tools/solve_run.py 100 480 4 $args > gpurun_out/x100_$i.log 2> gpurun_out/x100_${i}_v.log
+  echo "$args"; tail -1 gpurun_out/x100_$i.log | cut -c1-420
 done
