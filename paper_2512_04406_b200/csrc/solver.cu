@@ -105,11 +105,6 @@ static double now_s() {
   return duration<double>(steady_clock::now().time_since_epoch()).count();
 }
 
-static double stall_guard() {
-  static const double g = getenv("DRSDP_STALL_GUARD") ? atof(getenv("DRSDP_STALL_GUARD")) : 100.0;
-  return g;
-}
-
 struct Run {
   drsdp_ctx *ctx;
   SolverState *s;
@@ -322,7 +317,7 @@ struct Run {
       if (s->cur.gn <= 0.5 * best_gn) {
         best_gn = s->cur.gn;
         since_best = 0;
-      } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr && s->cur.gn <= stall_guard() * grad_tol) {
+      } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr && s->cur.gn <= 100.0 * grad_tol) {
         // stagnation exit only near the tolerance (reading R30): far from it the inner solve
         // keeps going (an inexact subproblem solution steers the ALM multiplier update wrongly)
         last_exit = 1;

@@ -1,7 +1,3 @@
 mkdir -p gpurun_out
-i=0
-for args in "escape_max=32" "mode=1" "escape_max=32 mode=1"; do
-  i=$((i+1))
-  DRSDP_VERBOSE=1 timeout 560 python tools/solve_run.py 100 480 4 $args > gpurun_out/x100_$i.log 2> gpurun_out/x100_${i}_v.log
-  echo "$args"; tail -1 gpurun_out/x100_$i.log | cut -c1-420
-done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pt_full.log 2>&1; tail -3 gpurun_out/pt_full.log
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc=$?"; tail -c 600 gpurun_out/bench_final.json
