@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pt_full.log 2>&1; tail -3 gpurun_out/pt_full.log
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo "bench rc=$?"; tail -c 600 gpurun_out/bench_final.json
+DRSDP_VERBOSE=1 timeout 3400 python tools/solve_run.py 150 3300 4 > gpurun_out/solve_r34_150_long.log 2> gpurun_out/solve_r34_150_long_v.log
+tail -1 gpurun_out/solve_r34_150_long.log | cut -c1-420
