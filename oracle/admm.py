@@ -188,6 +188,8 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
             trace.append(row)
             break
         Vs = escape_directions(res["lam"], res["V"], prm.eig_neg_tol, prm.escape_max)
+        if Vs is not None and Y.shape[1] + Vs.shape[1] > n:  # p never exceeds n (S has rank <= n)
+            Vs = Vs[:, : n - Y.shape[1]] if Y.shape[1] < n else None
         # rank tolerance tied to the residual (reading R32); no reduction in an iteration that
         # escapes (reading R34: the escape columns of the previous iteration are O(sqrt(|lambda|/sigma))
         # and a relative tolerance would remove them before they grow)
