@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-DRSDP_VERBOSE=1 timeout 2800 python tools/solve_run.py 100 2700 4 > gpurun_out/solve_r34_100_long.log 2> gpurun_out/solve_r34_100_long_v.log
-tail -1 gpurun_out/solve_r34_100_long.log | cut -c1-420
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+timeout 400 python tools/alm_profile.py 80 16,64,128,240 30 2>&1 | tail -6
+timeout 400 python tools/alm_profile.py 150 64,256,512 10 2>&1 | tail -4
