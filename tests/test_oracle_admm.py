@@ -130,16 +130,16 @@ def test_p_update_escape_xor_reduce():
 
 
 def test_residue_diving_behaviour():
-    """Reported, not gated by the paper (Fig. 3, single instances): the last outer
-    iteration drops log10 eta_max by >= 4 decades on at least one of 3 seeds (with the inexact
-    inner solves of readings R30/R33 the final drop at d = 10 is 0.9-10 decades by seed)."""
+    """Residue diving (Fig. 3): the last outer iteration drops
+    log10 eta_max by >= 4 decades on at least 2 of 3 q = 10 instances (measured with the
+    readings R30-R34: 7.9, 5.8 and 3.5 decades for seeds 0, 1, 2)."""
     dives = 0
     for seed in range(3):
         Q, c, amap, cnt, b, prm, Y0 = _solve(10, seed, p0=2)
         tr = admm.solve(amap, cnt, b, None, prm, Y0)["trace"]
         drop = np.log10(tr[-2]["eta_max"]) - np.log10(tr[-1]["eta_max"]) if len(tr) >= 2 else 0.0
         dives += drop >= 4
-    assert dives >= 1
+    assert dives >= 2
 
 
 def test_determinism():

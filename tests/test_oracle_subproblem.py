@@ -223,3 +223,73 @@ def test_alm_cost_forms_agree():
         assert abs(sp.alm_cost(T, amap, cnt, C, sigma, Y) - ref) <= 1e-12 * np.sum((S + C + T / sigma) ** 2)
         f, _, _ = sp.ALMProblem(T, amap, cnt, C, sigma).costgrad(Y)
         assert f == sp.alm_cost(T, amap, cnt, C, sigma, Y) or abs(f - ref) <= 1e-12 * abs(ref)
+
+
+# ---- pins of the row-sampled / blocked / RTR-callable copies ------------
+@pytest.mark.parametrize("p", [1, 16, 64])
+def test_fixed_rows_match_fixed_eval(p):
+    """fixed_rows (the checker of the n = 16384 / 32768 GPU tests and of the bench's
+    cpu_baseline) equals the FD-pinned fixed_eval row by row (E, rho, R, H)."""
+    n = 200
+    M = random_symmetric(n, 31 + p, 1.0 / np.sqrt(n))
+    Y = random_unit_factor(n, p, 32)
+    U = sp.project(Y, random_matrix(n, p, 33))
+    full = sp.fixed_eval(M, Y, U)
+    rows = np.array([0, 1, 7, 64, 127, 128, 150, 199])
+    part = sp.fixed_rows(M[rows], rows, Y, U)
+    for key in ("E", "R", "H"):
+        scale = max(1.0, np.abs(full[key]).max())
+        assert np.abs(part[key] - full[key][rows]).max() <= 1e-13 * scale, key
+    assert np.abs(part["rho"] - full["rho"][rows]).max() <= 1e-13 * max(1.0, np.abs(full["rho"]).max())
+
+
+@pytest.mark.parametrize("block", [1, 37, 64, 1024])
+def test_fixed_cost_blocked_matches_fixed_cost(block):
+    n, p = 150, 8
+    M = random_symmetric(n, 41, 0.2)
+    Y = random_unit_factor(n, p, 42)
+    ref = sp.fixed_eval(M, Y)["f"]
+    f = sp.fixed_cost_blocked(lambda i0, i1: M[i0:i1], Y, block)
+    assert abs(f - ref) <= 1e-13 * ref
+    assert abs(sp.fixed_cost(M, Y) - ref) <= 1e-13 * ref
+
+
+@pytest.mark.parametrize("with_C", [False, True])
+def test_alm_problem_matches_alm_eval(with_C):
+    """ALMProblem.costgrad / .hess (the copies RTR drives) equal the FD-pinned alm_eval:
+    f, R (costgrad) and H (hess at the cached point)."""
+    amap, cnt, b, D, Xt, T, sigma = _bqp_state(5, 9, sigma=2.5, lemma31=not with_C)
+    n = amap.shape[0]
+    C = random_symmetric(n, 91, 0.05) if with_C else None
+    prob = sp.ALMProblem(T, amap, cnt, C, sigma)
+    for s in range(2):
+        Y = random_unit_factor(n, 4, 92 + s)
+        U = sp.project(Y, random_matrix(n, 4, 94 + s))
+        ref = sp.alm_eval(T, amap, cnt, C, sigma, Y, U)
+        f, R, ctx = prob.costgrad(Y)
+        H = prob.hess(ctx, U)
+        assert abs(f - ref["f"]) <= 1e-13 * max(1.0, abs(ref["f"]))
+        assert np.abs(R - ref["R"]).max() <= 1e-12 * max(1.0, np.abs(ref["E"]).max())
+        assert np.abs(H - ref["H"]).max() <= 1e-12 * max(1.0, np.abs(ref["H"]).max())
+    assert prob.n_costgrad == 2 and prob.n_hvp == 2
+
+
+def test_alm_problem_taylor_slopes():
+    """ALMProblem itself passes the Taylor-slope checks (slope 2 for the gradient, 3 with the
+    Hessian term) with a nonzero C, independently of alm_eval."""
+    amap, cnt, b, D, Xt, T, sigma = _bqp_state(4, 12, sigma=1.7, lemma31=False)
+    n = amap.shape[0]
+    C = random_symmetric(n, 120, 0.05)
+    prob = sp.ALMProblem(T, amap, cnt, C, sigma)
+    Y = random_unit_factor(n, 3, 121)
+    U = sp.project(Y, random_matrix(n, 3, 122))
+
+    def cg(Yx):
+        f, R, _ = prob.costgrad(Yx)
+        return f, R
+
+    def hs(Yx, Ux):
+        _, _, ctx = prob.costgrad(Yx)
+        return prob.hess(ctx, Ux)
+
+    _fd_checks(cg, hs, Y, U)
