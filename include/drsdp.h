@@ -125,6 +125,9 @@ typedef struct {
                                           stall_rtr iterations and is within 100x of the inner
                                           tolerance (0 = never; reading R30)                       */
   int32_t reserved;
+  double precond_mu;                   /* truncated-CG preconditioner Prec(R) = P_Y(R W),
+                                          W = gbar (Y^T Y + mu gbar I)^{-1}, gbar = tr(Y^T Y)/p
+                                          (reading R35); 0 = unpreconditioned                    */
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);

@@ -54,6 +54,7 @@ class Params:
         self.rho_reg = 1e3
         self.stall_rtr = 10
         self.max_tcg = 100
+        self.precond_mu = 0.0  # reading R35: Gram right-preconditioner of the truncated CG (0 = off)
         for k, v in kw.items():
             if not hasattr(self, k):
                 raise TypeError(f"unknown parameter {k}")
@@ -158,7 +159,8 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         eps_k = max(0.1 * min(1.0, eta_prev) * prm.eps_scale, prm.eps_floor)  # ||XY|| scale
         grad_tol = 4.0 * eps_k / sigma  # f scale: ||XY|| = sigma/4 ||R||
         Y, info = rtr(prob, Y, RTRParams(n, p, max_iter=prm.max_rtr, rho_reg=prm.rho_reg,
-                                        max_tcg=prm.max_tcg if prm.max_tcg > 0 else None), grad_tol, warm_U=U,
+                                        max_tcg=prm.max_tcg if prm.max_tcg > 0 else None,
+                                        precond_mu=prm.precond_mu), grad_tol, warm_U=U,
                       stall=prm.stall_rtr)
         totals["rtr"] += info["iters"]
         totals["tcg"] += info["tcg"]

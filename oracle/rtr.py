@@ -19,7 +19,7 @@ from .subproblem import inner, project, retract
 
 class RTRParams:
     def __init__(self, n, p, max_iter=500, max_tcg=None, rho_prime=0.1, kappa=0.1, theta=1.0,
-                 delta_bar=None, delta0=None, rho_reg=1e3):
+                 delta_bar=None, delta0=None, rho_reg=1e3, precond_mu=0.0):
         self.delta_bar = math.sqrt(n) if delta_bar is None else delta_bar
         self.delta0 = self.delta_bar / 8.0 if delta0 is None else delta0
         self.rho_prime = rho_prime
@@ -28,10 +28,26 @@ class RTRParams:
         self.max_iter = max_iter
         self.max_tcg = max(1, n * (p - 1)) if max_tcg is None else max_tcg
         self.rho_reg = rho_reg
+        self.precond_mu = precond_mu
 
 
-def tcg(prob, ctx, Y, g, Delta, prm: RTRParams):
-    """Steihaug-Toint truncated CG on the model m(eta) = f + <g,eta> + 1/2 <eta, H eta>.
+def gram_preconditioner(Y, mu):
+    """Right preconditioner of the truncated CG (reading R35), an SPD operator on the
+    tangent space at Y:  Prec(R) = P_Y(R W),  W = gbar (G + mu gbar I)^{-1},  G = Y^T Y,
+    gbar = tr(G)/p.  Returns None (identity) when mu <= 0."""
+    if mu <= 0:
+        return None
+    G = Y.T @ Y
+    gbar = np.trace(G) / G.shape[0]
+    W = gbar * np.linalg.inv(G + mu * gbar * np.eye(G.shape[0]))
+    W = 0.5 * (W + W.T)
+    return lambda R: project(Y, R @ W)
+
+
+def tcg(prob, ctx, Y, g, Delta, prm: RTRParams, prec=None):
+    """Steihaug-Toint truncated CG on the model m(eta) = f + <g,eta> + 1/2 <eta, H eta>, with an
+    optional preconditioner prec (SPD on the tangent space; the trust region is then measured
+    in the norm <eta, prec^{-1} eta>, tracked by the e_Pe / e_Pd / d_Pd recurrences).
 
     Returns (eta, Heta, n_inner, hit_boundary)."""
     eta = np.zeros_like(Y)
@@ -39,15 +55,17 @@ def tcg(prob, ctx, Y, g, Delta, prm: RTRParams):
     r = g.copy()
     r_r = inner(r, r)
     norm_r0 = math.sqrt(r_r)
-    delta = -r
-    e_Pe, e_Pd, d_Pd = 0.0, 0.0, r_r
+    z = r if prec is None else prec(r)
+    z_r = inner(z, r)
+    delta = -z
+    e_Pe, e_Pd, d_Pd = 0.0, 0.0, z_r
     model = 0.0
     hit = False
     j = 0
     for j in range(1, prm.max_tcg + 1):
         Hdelta = prob.hess(ctx, delta)
         d_Hd = inner(delta, Hdelta)
-        alpha = r_r / d_Hd if d_Hd != 0 else math.inf
+        alpha = z_r / d_Hd if d_Hd != 0 else math.inf
         e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd
         if d_Hd <= 0 or e_Pe_new >= Delta * Delta:
             tau = (-e_Pd + math.sqrt(e_Pd * e_Pd + d_Pd * (Delta * Delta - e_Pe))) / d_Pd
@@ -62,14 +80,16 @@ def tcg(prob, ctx, Y, g, Delta, prm: RTRParams):
             break
         eta, Heta, model, e_Pe = new_eta, new_Heta, new_model, e_Pe_new
         r = r + alpha * Hdelta
-        r_r_old = r_r
         r_r = inner(r, r)
         if math.sqrt(r_r) <= norm_r0 * min(norm_r0 ** prm.theta, prm.kappa):
             break
-        beta = r_r / r_r_old
-        delta = project(Y, -r + beta * delta)
+        z = r if prec is None else prec(r)
+        z_r_old = z_r
+        z_r = inner(z, r)
+        beta = z_r / z_r_old
+        delta = project(Y, -z + beta * delta)
         e_Pd = beta * (e_Pd + alpha * d_Pd)
-        d_Pd = r_r + beta * beta * d_Pd
+        d_Pd = z_r + beta * beta * d_Pd
     return eta, Heta, j, hit
 
 
@@ -111,7 +131,7 @@ def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, 
             if stall > 0 and since_best > stall and gn <= 100.0 * grad_tol:
                 break
         info["iters"] += 1
-        eta, Heta, nin, hit = tcg(prob, ctx, Y, g, Delta, prm)
+        eta, Heta, nin, hit = tcg(prob, ctx, Y, g, Delta, prm, gram_preconditioner(Y, prm.precond_mu))
         info["tcg"] += nin
         try:
             Yp = retract(Y, eta)

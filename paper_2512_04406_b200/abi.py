@@ -40,7 +40,7 @@ class Params(C.Structure):
                 ("eps_floor", C.c_double), ("time_limit_s", C.c_double), ("p0", C.c_int32),
                 ("max_outer", C.c_int32), ("max_rtr", C.c_int32), ("max_tcg", C.c_int32),
                 ("escape_max", C.c_int32), ("mode", C.c_int32), ("seed", C.c_uint64), ("rho_reg", C.c_double),
-                ("stall_rtr", C.c_int32), ("reserved", C.c_int32)]
+                ("stall_rtr", C.c_int32), ("reserved", C.c_int32), ("precond_mu", C.c_double)]
 
 
 class Info(C.Structure):

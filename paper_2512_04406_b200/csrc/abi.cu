@@ -75,7 +75,7 @@ int choose_splits(drsdp_ctx *ctx, int krows, int ntiles) {
 int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
   (void)n;
   (void)p;
-  CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64 + 64), "alloc gram workspace");
+  CK(ctx->gram_part.ensure((size_t)296 * 2 * 64 * 64 + 2048), "alloc gram workspace");  // + final-kernel block partials
   return DRSDP_OK;
 }
 
@@ -302,6 +302,10 @@ static int small_right(drsdp_ctx *ctx, int n, int p, const double *A1, int lda, 
   a.out = W;
   a.ldo = ldw;
   return run_product(ctx, a, EPI_RAW, A2 ? MODE2_PAIR : MODE2_NONE, true, 0);
+}
+
+int right_product(drsdp_ctx *ctx, int n, int p, const double *A, int lda, const double *B, double *out, int ldo) {
+  return small_right(ctx, n, p, A, lda, B, nullptr, nullptr, out, ldo);
 }
 
 static int ensure_big(drsdp_ctx *ctx, int n, int ldv) {
@@ -570,8 +574,11 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
     CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0), "stream wait");
     ctx->stream = ctx->aux_stream;
   }
-  int rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, U, nullptr, K, nullptr)
-                  : gram(ctx, n, p, Y, ldv, U, ctx->sub_G.ptr, K, nullptr);
+  int rc = ctx->g_scratch.cap >= (size_t)p * p ? DRSDP_OK
+                                                : cuda_check(ctx, ctx->g_scratch.ensure((size_t)p * p), "alloc G");
+  if (rc) return rc;
+  rc = p > 64 ? gram_generic(ctx, n, p, Y, ldv, U, nullptr, K, nullptr)
+              : gram(ctx, n, p, Y, ldv, U, ctx->g_scratch.ptr, K, nullptr);
   if (fork) {
     ctx->stream = main_stream;
     if (rc) return rc;
@@ -612,8 +619,29 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
 // ----------------------------------------------------------------------------------------------
 // Problem construction
 // ----------------------------------------------------------------------------------------------
-static int finalize_problem(drsdp_ctx *ctx, const double *C_host) {
-  Problem &P = ctx->prob;
+// Validates the staged problem P (host arrays filled by set_problem / set_bqp), builds its CSR
+// segments and device copies, and only then replaces ctx->prob (releasing the previous problem's
+// device buffers). On any error ctx->prob is left untouched and P's partial allocations freed.
+static int finalize_staged(drsdp_ctx *ctx, Problem &P, const double *C_host);
+static int finalize_problem(drsdp_ctx *ctx, Problem &P, const double *C_host) {
+  const int rc = finalize_staged(ctx, P, C_host);
+  if (rc) {
+    P.release();
+    return rc;
+  }
+  ctx->has_problem = false;
+  ctx->prob.release();
+  ctx->prob = P;  // DBufs move by copy (no destructor); P is not used again
+  ctx->has_problem = true;
+  ctx->alm_cached_valid = false;
+  ctx->h_Y0.clear();  // an initial factor belongs to the problem it was given for
+  ctx->p0_given = 0;
+  free_solver(ctx);
+  ctx->trace.clear();
+  return DRSDP_OK;
+}
+
+static int finalize_staged(drsdp_ctx *ctx, Problem &P, const double *C_host) {
   const int64_t n = P.n, m = P.m;
   // counts, CSR over upper positions (constraint-major, row-major within a constraint)
   std::vector<int64_t> cnt_upper(m, 0);
@@ -697,10 +725,6 @@ static int finalize_problem(drsdp_ctx *ctx, const double *C_host) {
     CK(P.cA.ensure(m), "alloc cA");
     CK(cudaMemcpy(P.cA.ptr, cA.data(), sizeof(double) * m, cudaMemcpyHostToDevice), "copy cA");
   }
-  ctx->has_problem = true;
-  ctx->alm_cached_valid = false;
-  free_solver(ctx);
-  ctx->trace.clear();
   return DRSDP_OK;
 }
 
@@ -798,17 +822,7 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   free_solver(ctx);
-  Problem &P = ctx->prob;
-  P.amap.release();
-  P.C.release();
-  P.cA.release();
-  P.cnt.release();
-  P.b.release();
-  P.seg_ptr.release();
-  P.seg_pos.release();
-  P.is_large.release();
-  P.large_ids.release();
-  P.huge_ids.release();
+  ctx->prob.release();
   ctx->red_part.release();
   ctx->gram_part.release();
   ctx->symv_part.release();
@@ -825,6 +839,10 @@ void drsdp_destroy(drsdp_ctx *ctx) {
   ctx->sub_G.release();
   ctx->sub_K.release();
   ctx->sub_rho.release();
+  ctx->g_scratch.release();
+  ctx->alm_G.release();
+  ctx->alm_K.release();
+  ctx->alm_rho.release();
   ctx->alm_M.release();
   ctx->alm_yS.release();
   ctx->alm_wZ.release();
@@ -897,8 +915,7 @@ int drsdp_set_problem(drsdp_ctx *ctx, int64_t n, int64_t m, const double *C, int
   if (n <= 0 || n >= 65536 || m <= 0 || nnz < 0 || !b || (nnz > 0 && (!row || !col || !cons)))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_problem: bad sizes or NULL arrays");
   cudaSetDevice(ctx->device);
-  Problem &P = ctx->prob;
-  P = Problem();
+  Problem P;  // staged: ctx->prob is replaced only after validation succeeds
   P.n = n;
   P.m = m;
   P.h_amap.assign((size_t)n * n, -1);
@@ -917,8 +934,7 @@ int drsdp_set_problem(drsdp_ctx *ctx, int64_t n, int64_t m, const double *C, int
         if (C[i * n + j] != C[j * n + i]) return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_problem: C not symmetric");
   }
   P.h_b.assign(b, b + m);
-  ctx->has_problem = false;
-  return finalize_problem(ctx, C);
+  return finalize_problem(ctx, P, C);
 }
 
 int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c) {
@@ -930,8 +946,7 @@ int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c) {
       if (Q[i * d + j] != Q[j * d + i]) return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_bqp: Q not symmetric");
   cudaSetDevice(ctx->device);
   MonoRank mr(d);
-  Problem &P = ctx->prob;
-  P = Problem();
+  Problem P;  // staged (see finalize_problem)
   const int64_t n = 1 + d + (int64_t)d * (d - 1) / 2;
   P.n = n;
   P.m = mr.off[5];
@@ -982,8 +997,7 @@ int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c) {
       int a[2] = {i, j};
       P.h_b[mr.id(a, 2)] = 2.0 * Q[i * d + j];
     }
-  ctx->has_problem = false;
-  return finalize_problem(ctx, nullptr);
+  return finalize_problem(ctx, P, nullptr);
 }
 
 int drsdp_get_sizes(drsdp_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_upper) {
@@ -1029,6 +1043,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->seed = 0;
   o->rho_reg = 1e3;
   o->stall_rtr = 10;
+  o->precond_mu = 0.0;
   return DRSDP_OK;
 }
 
@@ -1038,7 +1053,7 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
-        q.rho_reg >= 0 && q.stall_rtr >= 0))
+        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.precond_mu >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;
   return DRSDP_OK;
@@ -1238,14 +1253,14 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   CK(ctx->alm_M.ensure((size_t)n * P.ld), "alloc M");
   CK(ctx->alm_yS.ensure(P.m), "alloc yS");
   CK(ctx->alm_wZ.ensure(P.m), "alloc wZ");
-  CK(ctx->sub_rho.ensure(n), "alloc rho");
-  CK(ctx->sub_G.ensure((size_t)2 * p * p), "alloc G");
-  CK(ctx->sub_K.ensure((size_t)p * p), "alloc K");
+  CK(ctx->alm_rho.ensure(n), "alloc rho");
+  CK(ctx->alm_G.ensure((size_t)2 * p * p), "alloc G");
+  CK(ctx->alm_K.ensure((size_t)p * p), "alloc K");
   int rc;
   if (flags & DRSDP_EVAL_COSTGRAD) {
     CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
-    rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->sub_G.ptr,
-                      ctx->sub_rho.ptr, cost_dev, egrad_dev, rgrad_dev, ctx->alm_D.ptr);
+    rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->alm_G.ptr,
+                      ctx->alm_rho.ptr, cost_dev, egrad_dev, rgrad_dev, ctx->alm_D.ptr);
     if (rc) return rc;
     ctx->alm_cached_valid = true;
     ctx->alm_cached_Y = Y_dev;
@@ -1258,7 +1273,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   }
   if (flags & DRSDP_EVAL_HVP) {
     CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
-    rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->sub_G.ptr, ctx->sub_K.ptr, ctx->sub_rho.ptr,
+    rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->alm_G.ptr, ctx->alm_K.ptr, ctx->alm_rho.ptr,
                  ctx->alm_wZ.ptr, hvp_dev, ctx->alm_Z.ptr);
     if (rc) return rc;
   }

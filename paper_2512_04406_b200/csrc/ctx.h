@@ -11,13 +11,22 @@
 
 namespace drsdp {
 
-// device buffer with grow-on-demand
+// Process-wide allocation epoch: bumped whenever a DBuf (re)allocates or frees device memory.
+// A captured CUDA graph bakes in every device address it touches, so a graph captured at an
+// older epoch may reference freed memory and must be re-captured (solver.cu, Graph::epoch).
+inline uint64_t &dbuf_epoch() {
+  static uint64_t e = 0;
+  return e;
+}
+
+// device buffer with grow-on-demand (no destructor: ownership is explicit, release() frees)
 template <typename T>
 struct DBuf {
   T *ptr = nullptr;
   size_t cap = 0;  // elements
   cudaError_t ensure(size_t n) {
     if (n <= cap) return cudaSuccess;
+    ++dbuf_epoch();
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     cap = 0;
@@ -33,6 +42,7 @@ struct DBuf {
     return cudaMemset(ptr, 0, cap * sizeof(T));
   }
   void release() {
+    if (ptr) ++dbuf_epoch();
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     cap = 0;
@@ -78,6 +88,18 @@ struct Problem {
   DBuf<uint8_t> is_large;
   DBuf<int32_t> large_ids, huge_ids;
   int64_t n_large = 0, n_huge = 0;
+  void release() {
+    amap.release();
+    C.release();
+    cA.release();
+    cnt.release();
+    b.release();
+    seg_ptr.release();
+    seg_pos.release();
+    is_large.release();
+    large_ids.release();
+    huge_ids.release();
+  }
 };
 
 struct SolverState;
@@ -122,12 +144,14 @@ struct drsdp_ctx {
   // fixed-M subproblem (borrowed)
   const double *sub_M = nullptr;
   int64_t sub_n = 0, sub_ldm = 0;
-  drsdp::DBuf<double> sub_G, sub_K, sub_rho;
+  drsdp::DBuf<double> sub_G, sub_K, sub_rho;  // fixed-M eval cache (drsdp_subproblem_eval only)
+  drsdp::DBuf<double> g_scratch;              // G recomputed as a by-product of K inside HVPs
   const double *sub_cached_Y = nullptr;
   int sub_cached_p = 0;
   bool sub_cached_valid = false;
   // ALM eval cache (ABI drsdp_alm_eval)
   drsdp::DBuf<double> alm_M, alm_yS, alm_wZ, alm_D, alm_Z;
+  drsdp::DBuf<double> alm_G, alm_K, alm_rho;  // ALM eval cache (separate from the fixed-M one)
   const double *alm_cached_Y = nullptr;
   const double *alm_cached_T = nullptr;
   int alm_cached_p = 0;
@@ -162,6 +186,8 @@ struct SymvArgs;
 int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind);
 int rowdot_product(drsdp_ctx *ctx, int n, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z,
                    double *zsum);
+// out (n x p, pitch ldo) = A (n x p, pitch lda) B (p x p, pitch p)
+int right_product(drsdp_ctx *ctx, int n, int p, const double *A, int lda, const double *B, double *out, int ldo);
 int apply_w_product(drsdp_ctx *ctx, int n, int p, const double *Y, int ldv, const double *W, int r, double *out,
                     int ldo);
 // fused subproblem evaluations on device pointers (pitch ldv for all n x p arrays)

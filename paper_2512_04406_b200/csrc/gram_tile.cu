@@ -13,6 +13,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "gram_tile.cuh"
 
 namespace drsdp {
@@ -26,36 +27,6 @@ constexpr int STAGE_ELEMS = 2 * OP_ELEMS;
 constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * 8 + 1024;
 
-DRSDP_DEV uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-DRSDP_DEV void bar_init(uint64_t *b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
-}
-DRSDP_DEV void bar_expect(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-DRSDP_DEV void bar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-DRSDP_DEV void bar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
-          su32(b)),
-      "r"(parity)
-      : "memory");
-}
-DRSDP_DEV void tma2d(void *dst, const CUtensorMap *m, int ci, int co, uint64_t *b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          su32(dst)),
-      "l"(m), "r"(ci), "r"(co), "r"(su32(b))
-      : "memory");
-}
-DRSDP_DEV double ldsw(uint32_t box, int row, int col) {
-  const uint32_t a = box + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
 }  // namespace
 
 __global__ void __launch_bounds__(NT, 1)
@@ -141,40 +112,12 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
-typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeFn encoder() {
-  static EncodeFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(f);
-    else
-      cudaGetLastError();
-  }
-  return fn;
-}
-
 static bool map_rows(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld) {
-  EncodeFn fn = encoder();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {16, (cuuint32_t)TB};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tma_map_f64(m, base, rows, cols, ld, TB);
 }
 
 bool gram_tile_supported(const double *A, const double *B, int ld) {
-  return !(ld & 1) && !((uintptr_t)A & 15) && !((uintptr_t)B & 15) && encoder() != nullptr;
+  return !(ld & 1) && !((uintptr_t)A & 15) && !((uintptr_t)B & 15) && tma_encoder() != nullptr;
 }
 
 cudaError_t gram_tile_launch(int n, int p, const double *A1, const double *B1, const double *A2, const double *B2,

@@ -93,27 +93,42 @@ __global__ void __launch_bounds__(256) gram_kernel(int n, int p, const double *_
   }
 }
 
-// second phase for large p x p results: thread e sums entry e over the nb block partials (in block
-// order), G / K written, ||G||^2 by a deterministic grid reduction
+// second phase: one warp per entry e; lane l sums the block partials l, l + 32, ... in order and
+// the warp combines the 32 lane sums with a fixed butterfly (deterministic). G / K written,
+// ||G||^2 by a deterministic grid reduction. (A single last block summing nb partials per entry
+// serially cost ~40 us at nb = 296: one dependent L2 round trip per partial.)
 __global__ void __launch_bounds__(256) gram_final_kernel(int nval, int pp, int nb, const double *__restrict__ part,
                                                          double *G, double *K, double *gg, double *red,
                                                          unsigned *counter, const int *skip) {
   if (skip && *(volatile const int *)skip) return;
   __shared__ double scratch[8];
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   double v[1] = {0.0};
   if (e < nval) {
-    const double s = ordered_sum(part + e, nb, (size_t)nval);
-    if (e < pp) {
-      G[e] = s;
-      v[0] = s * s;
-    } else {
-      K[e - pp] = s;
+    double s = 0.0;
+    int b = lane;
+    for (; b + 96 < nb; b += 128) {
+      const double t0 = __ldcg(part + (size_t)b * nval + e), t1 = __ldcg(part + (size_t)(b + 32) * nval + e);
+      const double t2 = __ldcg(part + (size_t)(b + 64) * nval + e), t3 = __ldcg(part + (size_t)(b + 96) * nval + e);
+      s += t0;
+      s += t1;
+      s += t2;
+      s += t3;
+    }
+    for (; b < nb; b += 32) s += __ldcg(part + (size_t)b * nval + e);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (e < pp) {
+        G[e] = s;
+        v[0] = s * s;
+      } else {
+        K[e - pp] = s;
+      }
     }
   }
   grid_sum<1>(v, red, counter, gg, scratch);
 }
-
 cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
   const int nval = a.U ? 2 * a.p * a.p : a.p * a.p;
   if (nval > 32 * 256) return cudaErrorInvalidValue;
@@ -123,16 +138,16 @@ cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
   int rpb = (a.n + nb - 1) / nb;
   nb = (a.n + rpb - 1) / rpb;
   const size_t smem = (size_t)2 * 32 * a.p * 8;
-  // large results: the single last block would sum nb x nval partials serially (~10 us per entry
-  // at nb = 296); a second kernel spreads that over nval threads
-  const int split_final = nval > 1024 ? 1 : 0;
+  // the partials are summed by a second kernel, one warp per entry (gram_final_kernel), unless
+  // there are only a few blocks
+  const int split_final = nb > 8 ? 1 : 0;
   gram_kernel<<<nb, 256, smem, st>>>(a.n, a.p, a.Y, a.ldy, a.U, a.ldu, rpb, a.part, a.counter, a.G, a.K, a.gg,
                                      a.skip, split_final);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || !split_final) return e;
   double *red = a.part + (size_t)nb * nval;
-  gram_final_kernel<<<(nval + 255) / 256, 256, 0, st>>>(nval, a.p * a.p, nb, a.part, a.G, a.K, a.gg, red, a.counter,
-                                                        a.skip);
+  gram_final_kernel<<<(nval + 7) / 8, 256, 0, st>>>(nval, a.p * a.p, nb, a.part, a.G, a.K, a.gg, red, a.counter,
+                                                    a.skip);
   return cudaGetLastError();
 }
 
@@ -681,8 +696,10 @@ __global__ void __launch_bounds__(256) normalize_rows_kernel(int n, int r, int l
 // ----------------------------------------------------------------------------------------------
 // Device-resident truncated CG (Steihaug-Toint, the recurrences of oracle/rtr.py tcg).
 // ----------------------------------------------------------------------------------------------
-__global__ void tcg_init_kernel(TcgDev *st, double gnorm, double Delta, int max_iters) {
+__global__ void tcg_init_kernel(TcgDev *st, double gnorm, double Delta, int max_iters, int prec) {
   if (threadIdx.x) return;
+  st->prec = prec;
+  st->z_r = gnorm * gnorm;  // prec: replaced by <Prec(r), r> (tcg_prec_kernel, init)
   st->r_r = gnorm * gnorm;
   st->norm_r0 = gnorm;
   st->e_Pe = 0.0;
@@ -707,7 +724,7 @@ __global__ void tcg_init_kernel(TcgDev *st, double gnorm, double Delta, int max_
 // block applies the acceptance / stopping rules. With use_cond it also drives the conditional
 // WHILE node of the captured graph (keep looping while the tCG runs).
 __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, TcgDev *st, double *e0, double *e1,
-                                                         double *h0, double *h1, double *r0, double *r1,
+                                                         double *h0, double *h1, double *r,
                                                          const double *__restrict__ d, const double *__restrict__ hd,
                                                          const double *__restrict__ g, double *part,
                                                          unsigned *counter, const double *kappa,
@@ -722,14 +739,18 @@ __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, T
     }
     return;
   }
-  const double r_r = st->r_r, e_Pe = st->e_Pe, e_Pd = st->e_Pd, d_Pd = st->d_Pd, Delta2 = st->Delta2;
-  const double alpha = dHd != 0.0 ? r_r / dHd : INFINITY;
+  const double r_r = st->r_r, z_r = st->z_r, e_Pe = st->e_Pe, e_Pd = st->e_Pd, d_Pd = st->d_Pd;
+  const double Delta2 = st->Delta2;
+  const int prec = st->prec;
+  const double alpha = dHd != 0.0 ? (prec ? z_r : r_r) / dHd : INFINITY;
   const double e_Pe_new = e_Pe + 2.0 * alpha * e_Pd + alpha * alpha * d_Pd;
   const int bnd = (dHd <= 0.0 || e_Pe_new >= Delta2) ? 1 : 0;
   const double a = bnd ? (-e_Pd + sqrt(e_Pd * e_Pd + d_Pd * (Delta2 - e_Pe))) / d_Pd : alpha;
   const int par = st->par;
-  const double *e = par ? e1 : e0, *h = par ? h1 : h0, *r = par ? r1 : r0;
-  double *eo = par ? e0 : e1, *ho = par ? h0 : h1, *ro = par ? r0 : r1;
+  // eta and H eta ping-pong (a rejected step keeps the previous ones); r is updated in place
+  // (it is only needed while the tCG continues)
+  const double *e = par ? e1 : e0, *h = par ? h1 : h0;
+  double *eo = par ? e0 : e1, *ho = par ? h0 : h1;
   double v[3] = {0.0, 0.0, 0.0};
   ROW_LOOP_BEGIN
   const size_t o = (size_t)row * ld;
@@ -744,7 +765,7 @@ __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, T
     v[1] = fma(ev, hv, v[1]);
     if (!bnd) {
       const double rv = fma(a, hdv, r[k]);
-      ro[k] = rv;
+      r[k] = rv;
       v[2] = fma(rv, rv, v[2]);
     }
   }
@@ -768,6 +789,9 @@ __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, T
       st->r_r = v[2];
       if (sqrt(v[2]) <= st->norm_r0 * fmin(st->norm_r0, 0.1)) {  // theta = 1, kappa = 0.1
         st->done = 1;
+      } else if (prec) {
+        // beta, e_Pd, d_Pd need <Prec(r), r>: tcg_prec_kernel after the preconditioner product
+        if (st->iters >= st->max_iters) st->done = 1;
       } else {
         const double beta = v[2] / r_r;
         st->e_Pd = beta * (e_Pd + a * d_Pd);
@@ -780,11 +804,10 @@ __global__ void __launch_bounds__(256) tcg_update_kernel(int n, int p, int ld, T
   if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
 }
 
+// delta = P_Y(-src + beta delta), src = r (or Prec(r) when preconditioned)
 __global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, const TcgDev *st,
-                                                         const double *__restrict__ Y, const double *r0,
-                                                         const double *r1, double *d) {
+                                                         const double *__restrict__ Y, const double *r, double *d) {
   if (*(volatile const int *)&st->done) return;
-  const double *r = st->par ? r1 : r0;
   const double beta = st->beta;
   ROW_LOOP_BEGIN
   const size_t o = (size_t)row * ld;
@@ -793,6 +816,65 @@ __global__ void __launch_bounds__(256) tcg_newdir_kernel(int n, int p, int ld, c
   s = warp_sum(s);
   for (int c = lane; c < p; c += 32) d[o + c] = fma(beta, d[o + c], -r[o + c]) - s * Y[o + c];
   ROW_LOOP_END
+}
+
+// Preconditioned tCG (reading R35; oracle/rtr.py tcg with prec): z holds r W on entry (W the
+// Gram preconditioner, tcg_prec_matrix_kernel); z <- P_Y(z) in place and <z, r> by a fixed-order
+// grid reduction. init: delta = -z and z_r = d_Pd = <z, r>. Otherwise the last block forms
+// beta = <z, r> / z_r_old and the recurrences e_Pd = beta (e_Pd + alpha d_Pd),
+// d_Pd = <z, r> + beta^2 d_Pd (the trust region is measured in the Prec^{-1} norm).
+__global__ void __launch_bounds__(256) tcg_prec_kernel(int n, int p, int ld, TcgDev *st, const double *__restrict__ Y,
+                                                       double *z, const double *__restrict__ r, double *d,
+                                                       double *part, unsigned *counter, int init) {
+  if (*(volatile const int *)&st->done) return;
+  __shared__ double scratch[8];
+  double v[1] = {0.0};
+  ROW_LOOP_BEGIN
+  const size_t o = (size_t)row * ld;
+  double s = 0.0;
+  for (int c = lane; c < p; c += 32) s = fma(z[o + c], Y[o + c], s);
+  s = warp_sum(s);
+  double zr = 0.0;
+  for (int c = lane; c < p; c += 32) {
+    const double zv = z[o + c] - s * Y[o + c];
+    z[o + c] = zv;
+    zr = fma(zv, r[o + c], zr);
+    if (init) d[o + c] = -zv;
+  }
+  zr = warp_sum(zr);
+  if (lane == 0) v[0] = zr;
+  ROW_LOOP_END
+  if (!grid_sum<1>(v, part, counter, nullptr, scratch) || threadIdx.x != 0) return;
+  const double zr = v[0];
+  if (init) {
+    st->z_r = zr;
+    st->d_Pd = zr;
+    return;
+  }
+  const double beta = zr / st->z_r;
+  st->e_Pd = beta * (st->e_Pd + st->alpha * st->d_Pd);
+  st->d_Pd = zr + beta * beta * st->d_Pd;
+  st->z_r = zr;
+  st->beta = beta;
+}
+
+// A = G / gbar + mu I and B = I (p x p, pitch p), gbar = tr(G) / p: the Cholesky solve A W = I
+// (cuSOLVER potrf / potrs on p x p) then gives the preconditioner matrix W = gbar (G + mu gbar I)^-1.
+__global__ void __launch_bounds__(256) tcg_prec_matrix_kernel(int p, const double *__restrict__ G, double mu,
+                                                              double *A, double *B) {
+  __shared__ double scratch[8];
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < p; i += blockDim.x) v[0] += G[(size_t)i * p + i];
+  block_sum<1>(v, scratch);
+  __shared__ double s_inv;
+  if (threadIdx.x == 0) s_inv = v[0] > 0.0 ? (double)p / v[0] : 1.0;
+  __syncthreads();
+  const double inv = s_inv;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e / p, j = e - i * p;
+    A[e] = G[e] * inv + (i == j ? mu : 0.0);
+    B[e] = i == j ? 1.0 : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(256) tcg_finalize_kernel(int n, int p, int ld, const TcgDev *st, double *e0,
@@ -900,21 +982,30 @@ cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, cudaStream_t s) {
-  tcg_init_kernel<<<1, 32, 0, s>>>(st, gnorm, Delta, max_iters);
+cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, int prec, cudaStream_t s) {
+  tcg_init_kernel<<<1, 32, 0, s>>>(st, gnorm, Delta, max_iters, prec);
   return cudaGetLastError();
 }
 cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
-                              double *r0, double *r1, const double *d, const double *hd, const double *g,
-                              double *part, unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond,
-                              int use_cond, cudaStream_t s) {
-  tcg_update_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1, r0, r1, d, hd, g, part, counter,
-                                                 kappa, cond, use_cond);
+                              double *r, const double *d, const double *hd, const double *g, double *part,
+                              unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond, int use_cond,
+                              cudaStream_t s) {
+  tcg_update_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, e0, e1, h0, h1, r, d, hd, g, part, counter, kappa,
+                                                 cond, use_cond);
   return cudaGetLastError();
 }
-cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
-                              const double *r1, double *d, cudaStream_t s) {
-  tcg_newdir_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, Y, r0, r1, d);
+cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *src, double *d,
+                              cudaStream_t s) {
+  tcg_newdir_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, Y, src, d);
+  return cudaGetLastError();
+}
+cudaError_t tcg_prec_launch(int n, int p, int ld, TcgDev *st, const double *Y, double *z, const double *r, double *d,
+                            double *part, unsigned *counter, int init, cudaStream_t s) {
+  tcg_prec_kernel<<<rows_grid(n), 256, 0, s>>>(n, p, ld, st, Y, z, r, d, part, counter, init);
+  return cudaGetLastError();
+}
+cudaError_t tcg_prec_matrix_launch(int p, const double *G, double mu, double *A, double *B, cudaStream_t s) {
+  tcg_prec_matrix_kernel<<<1, 256, 0, s>>>(p, G, mu, A, B);
   return cudaGetLastError();
 }
 

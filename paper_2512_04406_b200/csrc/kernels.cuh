@@ -125,21 +125,29 @@ struct TcgDev {
   int par;       // which of the ping-pong buffers (0/1) holds eta, H eta, r
   int boundary;  // this iteration steps to the boundary
   int max_iters;
+  int prec;      // preconditioned (reading R35): alpha, beta from z_r = <Prec(r), r>
+  double z_r;
 };
-cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, cudaStream_t s);
+cudaError_t tcg_init_launch(TcgDev *st, double gnorm, double Delta, int max_iters, int prec, cudaStream_t s);
 // after H delta: kappa = <delta, H delta> (device scalar) -> alpha or the boundary step tau;
 // eta' = eta + alpha delta, (H eta)' = H eta + alpha H delta, r' = r + alpha H delta, then the
 // model / residual decisions (last block); use_cond: also set the graph's WHILE condition
 cudaError_t tcg_update_launch(int n, int p, int ld, TcgDev *st, double *e0, double *e1, double *h0, double *h1,
-                              double *r0, double *r1, const double *d, const double *hd, const double *g,
-                              double *part, unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond,
-                              int use_cond, cudaStream_t s);
+                              double *r, const double *d, const double *hd, const double *g, double *part,
+                              unsigned *counter, const double *kappa, cudaGraphConditionalHandle cond, int use_cond,
+                              cudaStream_t s);
 // move the result into buffer 0 (eta, H eta) when it ended in buffer 1
 cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *e0, const double *e1, double *h0,
                                 const double *h1, cudaStream_t s);
-// delta = P_Y(-r + beta delta) in place
-cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *r0,
-                              const double *r1, double *d, cudaStream_t s);
+// delta = P_Y(-src + beta delta) in place (src = r, or z = Prec(r) when preconditioned)
+cudaError_t tcg_newdir_launch(int n, int p, int ld, const TcgDev *st, const double *Y, const double *src, double *d,
+                              cudaStream_t s);
+// preconditioned tCG (reading R35): z (= r W on entry) <- P_Y(z), z_r = <z, r>; init: delta = -z,
+// else beta and the e_Pd / d_Pd recurrences (see kernels.cu)
+cudaError_t tcg_prec_launch(int n, int p, int ld, TcgDev *st, const double *Y, double *z, const double *r, double *d,
+                            double *part, unsigned *counter, int init, cudaStream_t s);
+// A = G / gbar + mu I, B = I (gbar = tr(G)/p): inputs of the Cholesky solve giving W = A^{-1}
+cudaError_t tcg_prec_matrix_launch(int p, const double *G, double mu, double *A, double *B, cudaStream_t s);
 cudaError_t rowdot_launch(int n, int p, const double *P, int ldp, const double *Y, int ldy, double *z, double *part,
                           unsigned *counter, double *out, cudaStream_t st);
 cudaError_t normalize_rows_launch(int n, int r, int ld, double *X, cudaStream_t st);

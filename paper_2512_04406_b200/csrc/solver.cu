@@ -52,6 +52,7 @@ struct SolverState {
   DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2], Dbuf[2], Zbuf;
   DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
   DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
+  DBuf<double> Apre, Wpre, pwork;  // tCG preconditioner (reading R35): A = G/gbar + mu I, W = A^{-1}
   DBuf<int> devinfo;
   DBuf<double> work, gwork;
   DBuf<TcgDev> tcg;              // device-resident tCG scalars
@@ -61,6 +62,7 @@ struct SolverState {
   struct Graph {
     const double *Y = nullptr;
     int p = -1, ldp = -1;
+    uint64_t epoch = 0;  // dbuf_epoch() at capture: any (re)allocation since then invalidates
     bool warm = false, failed = false;  // failed: graph capture unsupported, use batched launches
     cudaGraphExec_t exec = nullptr;
   } graphs[2];
@@ -87,7 +89,7 @@ void free_solver(drsdp_ctx *ctx) {
   s->Zbuf.release();
   DBuf<double> *bs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw,
                         &s->tmp, &s->K, &s->wZ, &s->T, &s->X, &s->W, &s->ystar, &s->z, &s->Vst, &s->Wsmall,
-                        &s->work, &s->Geig, &s->Gw, &s->gwork};
+                        &s->work, &s->Geig, &s->Gw, &s->gwork, &s->Apre, &s->Wpre, &s->pwork};
   for (auto *b : bs) b->release();
   s->devinfo.release();
   s->tcg.release();
@@ -136,7 +138,7 @@ struct Run {
   int hvp_at(Point &P, int p, const double *U, double *H) {
     if (!fixed_mode()) return alm_hvp(ctx, p, P.M, s->ld, P.Y, s->ldp, U, P.G, s->K.ptr, P.rho, s->wZ.ptr, H, s->Zbuf.ptr);
     return eval_fixed(ctx, DRSDP_EVAL_HVP, n, p, s->Mbuf[0].ptr, s->ld, P.Y, s->ldp, U, nullptr, nullptr, nullptr, H,
-                      ctx->sub_G.ptr, s->K.ptr, P.rho, nullptr, true);
+                      ctx->g_scratch.ptr, s->K.ptr, P.rho, nullptr, true);
   }
   int dots(double *out3, const double *A0, const double *B0, const double *A1, const double *B1, const double *A2,
            const double *B2, int p) {
@@ -159,11 +161,19 @@ struct Run {
     Point &C = s->cur;
     TcgDev *st = s->tcg.ptr;
     RC(hvp_at(C, p, s->delta.ptr, s->Hdelta.ptr));
-    KL(tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr, s->r.ptr, s->r2.ptr,
+    KL(tcg_update_launch(n, p, s->ldp, st, s->eta.ptr, s->eta2.ptr, s->Heta.ptr, s->Heta2.ptr, s->r.ptr,
                          s->delta.ptr, s->Hdelta.ptr, C.R, ctx->red_part.ptr, ctx->counters + C_VEC,
                          ctx->d_scal + S_SCAL, cond, use_cond, ctx->stream),
        "tcg update");
-    KL(tcg_newdir_launch(n, p, s->ldp, st, C.Y, s->r.ptr, s->r2.ptr, s->delta.ptr, ctx->stream), "tcg newdir");
+    if (precond()) {
+      // z = P_Y(r W) (s->r2 holds z), beta from <z, r> (reading R35)
+      RC(right_product(ctx, n, p, s->r.ptr, s->ldp, s->Wpre.ptr, s->r2.ptr, s->ldp));
+      KL(tcg_prec_launch(n, p, s->ldp, st, C.Y, s->r2.ptr, s->r.ptr, s->delta.ptr, ctx->red_part.ptr,
+                         ctx->counters + C_VEC, 0, ctx->stream),
+         "tcg prec");
+    }
+    KL(tcg_newdir_launch(n, p, s->ldp, st, C.Y, precond() ? s->r2.ptr : s->r.ptr, s->delta.ptr, ctx->stream),
+       "tcg newdir");
     return DRSDP_OK;
   }
 
@@ -211,6 +221,23 @@ struct Run {
     return DRSDP_OK;
   }
 
+  bool precond() const { return prm.precond_mu > 0.0; }
+  // W = gbar (G + mu gbar I)^{-1} at the current point: A = G/gbar + mu I (kernel), Cholesky
+  // A = L L^T and W = A^{-1} by potrs on the identity (cuSOLVER, p x p); info checked with the
+  // trust-region step's read-back
+  int prec_matrix(int p) {
+    KL(tcg_prec_matrix_launch(p, s->cur.G, prm.precond_mu, s->Apre.ptr, s->Wpre.ptr, ctx->stream), "prec matrix");
+    const int lw = (int)s->pwork.cap - 1;
+    if (cusolverDnDpotrf(s->sol, CUBLAS_FILL_MODE_LOWER, p, s->Apre.ptr, p, s->pwork.ptr, lw, s->devinfo.ptr) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDpotrf");
+    if (cusolverDnDpotrs(s->sol, CUBLAS_FILL_MODE_LOWER, p, p, s->Apre.ptr, p, s->Wpre.ptr, p, s->devinfo.ptr) !=
+        CUSOLVER_STATUS_SUCCESS)
+      return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDpotrs");
+    ctx->launches += 2;
+    return DRSDP_OK;
+  }
+
   int tcg(int p, double Delta, int max_tcg) {
     Point &C = s->cur;
     const size_t bytes = (size_t)n * s->ldp * 8;
@@ -218,14 +245,25 @@ struct Run {
     CK(cudaMemsetAsync(s->Heta.ptr, 0, bytes, ctx->stream), "memset");
     CK(cudaMemcpyAsync(s->r.ptr, C.R, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "copy");
     CK(cudaMemsetAsync(s->delta.ptr, 0, bytes, ctx->stream), "memset");
-    KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, 0.0, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
-                     ctx->d_scal + S_DOTS, ctx->stream),
-       "newdir");
     TcgDev *st = s->tcg.ptr;
-    KL(tcg_init_launch(st, C.gn, Delta, max_tcg, ctx->stream), "tcg init");
+    KL(tcg_init_launch(st, C.gn, Delta, max_tcg, precond() ? 1 : 0, ctx->stream), "tcg init");
+    if (precond()) {
+      // z_0 = Prec(g), delta_0 = -z_0, z_r = d_Pd = <z_0, g>
+      RC(prec_matrix(p));
+      RC(right_product(ctx, n, p, s->r.ptr, s->ldp, s->Wpre.ptr, s->r2.ptr, s->ldp));
+      KL(tcg_prec_launch(n, p, s->ldp, st, C.Y, s->r2.ptr, s->r.ptr, s->delta.ptr, ctx->red_part.ptr,
+                         ctx->counters + C_VEC, 1, ctx->stream),
+         "tcg prec");
+    } else {
+      KL(newdir_launch(n, p, s->ldp, C.Y, s->r.ptr, 0.0, s->delta.ptr, ctx->red_part.ptr, ctx->counters + C_VEC,
+                       ctx->d_scal + S_DOTS, ctx->stream),
+         "newdir");
+    }
     const bool graphs_ok = !ctx->prof_on && std::getenv("DRSDP_NO_GRAPH") == nullptr;
     SolverState::Graph &g = s->graphs[C.Y == s->Ybuf[0].ptr ? 0 : 1];
-    if (g.Y != C.Y || g.p != p || g.ldp != s->ldp) {
+    if (g.Y != C.Y || g.p != p || g.ldp != s->ldp || (g.exec && g.epoch != dbuf_epoch())) {
+      // a new point buffer / rank / pitch, or device memory the graph references was reallocated
+      // since capture (workspaces grow with p): drop the graph and warm up again
       g.Y = C.Y;
       g.p = p;
       g.ldp = s->ldp;
@@ -233,7 +271,10 @@ struct Run {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       g.exec = nullptr;
     }
-    if (graphs_ok && g.warm && !g.exec && !g.failed) RC(capture_graph(g, p));
+    if (graphs_ok && g.warm && !g.exec && !g.failed) {
+      RC(capture_graph(g, p));
+      g.epoch = dbuf_epoch();
+    }
     if (graphs_ok && g.exec) {
       CK(cudaGraphLaunch(g.exec, ctx->stream), "graph launch");
       ctx->launches += 1;
@@ -337,7 +378,11 @@ struct Run {
       int flag = 0;
       CK(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read flag");
       CK(cudaMemcpyAsync(s->h_tcg, s->tcg.ptr, sizeof(TcgDev), cudaMemcpyDeviceToHost, ctx->stream), "read tcg");
+      int pinfo = 0;
+      if (precond())
+        CK(cudaMemcpyAsync(&pinfo, s->devinfo.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read info");
       RC(read_scalars(ctx, 0, S_DOTS + 3));
+      if (pinfo != 0) return set_error(ctx, DRSDP_ERR_NUMERIC, "preconditioner Cholesky failed");
       if (s->h_tcg->done == 2) return set_error(ctx, DRSDP_ERR_NUMERIC, "non-finite curvature");
       const int nin = s->h_tcg->iters;
       const bool hit = s->h_tcg->hit != 0;
@@ -415,13 +460,18 @@ static int set_pitch(drsdp_ctx *ctx, int ldp_new, bool keep_cur, int p) {
   CK(s->Wsmall.ensure(pp), "alloc W");
   CK(s->Geig.ensure(pp), "alloc");
   CK(s->Gw.ensure(ldp_new), "alloc");
-  CK(ctx->sub_G.ensure(2 * pp), "alloc G");
-  CK(ctx->sub_K.ensure(pp), "alloc K");
+  CK(ctx->g_scratch.ensure(2 * pp), "alloc G");
   int lw = 0;
   if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ldp_new, s->Geig.ptr,
                                   ldp_new, s->Gw.ptr, &lw) != CUSOLVER_STATUS_SUCCESS)
     return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd_bufferSize (Gram)");
   CK(s->gwork.ensure((size_t)lw + 1), "alloc");
+  CK(s->Apre.ensure(pp), "alloc");
+  CK(s->Wpre.ensure(pp), "alloc");
+  if (cusolverDnDpotrf_bufferSize(s->sol, CUBLAS_FILL_MODE_LOWER, ldp_new, s->Apre.ptr, ldp_new, &lw) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDpotrf_bufferSize");
+  CK(s->pwork.ensure((size_t)lw + 1), "alloc");
   s->ldp = ldp_new;
   assign_points(s);
   for (auto &g : s->graphs) g.p = -1;  // buffers moved: recapture
@@ -529,6 +579,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   const double t0 = now_s();
   const bool verbose = std::getenv("DRSDP_VERBOSE") != nullptr;
   const drsdp_params &prm = ctx->prm;
+  if (ctx->p0_given && ctx->h_Y0.size() != (size_t)ctx->prob.n * ctx->p0_given)
+    return set_error(ctx, DRSDP_ERR_STATE, "initial factor does not match the problem size");
   int p = ctx->p0_given ? ctx->p0_given : prm.p0;
   RC(alloc_solver(ctx, p));
   SolverState *s = ctx->solver;
@@ -661,7 +713,11 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       ctx->launches++;
     }
     CK(cudaMemcpyAsync(lam.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
+    int eig_info = 0;
+    CK(cudaMemcpyAsync(&eig_info, s->devinfo.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read info");
     RC(read_scalars(ctx, S_DUAL, 8));
+    if (eig_info != 0)
+      return set_error(ctx, DRSDP_ERR_NUMERIC, "eigen-decomposition of X failed (dsyevd info " + std::to_string(eig_info) + ")");
     const double R_norm = std::sqrt(std::max(0.0, ctx->h_scal[S_DUAL]));
     const double CT = ctx->h_scal[S_DUAL + 2];
     const double zsum = ctx->h_scal[S_ZSUM];
@@ -711,7 +767,11 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       std::vector<double> w(p), V((size_t)p * p);
       CK(cudaMemcpyAsync(w.data(), s->Gw.ptr, sizeof(double) * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
       CK(cudaMemcpyAsync(V.data(), s->Geig.ptr, sizeof(double) * p * p, cudaMemcpyDeviceToHost, ctx->stream), "read");
+      int g_info = 0;
+      CK(cudaMemcpyAsync(&g_info, s->devinfo.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read info");
       CK(cudaStreamSynchronize(ctx->stream), "sync");
+      if (g_info != 0)
+        return set_error(ctx, DRSDP_ERR_NUMERIC, "eigen-decomposition of Y^T Y failed (dsyevd info " + std::to_string(g_info) + ")");
       int r = 0;
       for (int i = 0; i < p; ++i)
         if (w[i] > rtol * rtol * w[p - 1]) ++r;

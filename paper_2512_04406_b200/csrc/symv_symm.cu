@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "symv.cuh"
 #include "tile_epilogue.cuh"
 
@@ -30,38 +31,6 @@ namespace {
 
 constexpr int BM = 128, BK = 32, NCW = 8, NTA = (NCW + 1) * 32, NTB = 256;
 constexpr int UNIT_TILES = 8;  // L: tiles per unit
-
-DRSDP_DEV uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-DRSDP_DEV void bar_init(uint64_t *b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
-}
-DRSDP_DEV void bar_expect(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-DRSDP_DEV void bar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-DRSDP_DEV void bar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
-          su32(b)),
-      "r"(parity)
-      : "memory");
-}
-DRSDP_DEV void tma2d(void *dst, const CUtensorMap *m, int ci, int co, uint64_t *b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          su32(dst)),
-      "l"(m), "r"(ci), "r"(co), "r"(su32(b))
-      : "memory");
-}
-// element (row, col) of a [rows][16] fp64 box with SWIZZLE_128B
-DRSDP_DEV double ldsw(uint32_t box, int row, int col) {
-  const uint32_t a = box + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
 
 template <int PT>
 struct SCfg {
@@ -236,36 +205,8 @@ __global__ void __launch_bounds__(NTB) symm_reduce_kernel(SymvArgs a, const doub
 }
 
 // ----------------------------------------------------------------------------------------------
-typedef CUresult (*EncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeFn encoder() {
-  static EncodeFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(f);
-    else
-      cudaGetLastError();
-  }
-  return fn;
-}
-
 static bool map2d(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
-  EncodeFn fn = encoder();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tma_map_f64(m, base, rows, cols, ld, box_rows);
 }
 
 int symm_units(int n, std::vector<int> &host_units, std::vector<int> &host_ustart) {
@@ -326,7 +267,7 @@ bool symm_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
   // doubled DMMA work per byte makes this variant DMMA/shared-memory bound (1.69 ms vs 1.37 ms)
   static const bool p16 = std::getenv("DRSDP_SYMM16") != nullptr;  // experiment: p <= 16
   return mode2 == MODE2_NONE && !atr && (a.k == 0 || a.k == a.n) && a.p <= (p16 ? 16 : 8) && a.A2 == nullptr &&
-         !(a.lda & 1) && !((uintptr_t)a.A & 15) && encoder() != nullptr && (epi != EPI_RAW || a.p <= 16);
+         !(a.lda & 1) && !((uintptr_t)a.A & 15) && tma_encoder() != nullptr && (epi != EPI_RAW || a.p <= 16);
 }
 
 cudaError_t symm_launch(const SymvArgs &a, int epi, double *Vt, int64_t ldvt, const int4 *units, int n_units,

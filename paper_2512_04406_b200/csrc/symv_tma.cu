@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 #include "symv.cuh"
 #include "tile_epilogue.cuh"
 
@@ -29,46 +30,6 @@ namespace {
 
 constexpr int BM = 128, BK = 32, NCW = 8;  // rows per CTA, k per stage, consumer warps
 constexpr int NTHREADS = (NCW + 1) * 32;
-
-DRSDP_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-DRSDP_DEV void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-DRSDP_DEV void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-DRSDP_DEV void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-DRSDP_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-DRSDP_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c_inner, int c_outer, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c_inner), "r"(c_outer), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// element (row, col) of a [rows][16] fp64 box written by TMA with SWIZZLE_128B (1024 B aligned):
-// the 16-byte chunk index (col / 2) is XORed with row % 8
-// (explicit ld.shared on a 32-bit shared address: a generic pointer would compile to LD.E)
-DRSDP_DEV double lds_sw(uint32_t box, int row, int col) {
-  const uint32_t a = box + row * 128 + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
 
 template <int PT>
 struct Cfg {
@@ -121,8 +82,8 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], NCW);
+      bar_init(&full_bar[s], 1);
+      bar_init(&empty_bar[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -139,7 +100,7 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
     if (lane == 0) {
       for (int kt = 0; kt < nk; ++kt) {
         const int st = kt % C::STAGES;
-        if (kt >= C::STAGES) mbar_wait(&empty_bar[st], ((kt / C::STAGES) - 1) & 1);
+        if (kt >= C::STAGES) bar_wait(&empty_bar[st], ((kt / C::STAGES) - 1) & 1);
         double *sa = smem + st * C::STAGE_ELEMS;
         double *sv = sa + C::A_ELEMS;
         int k0 = kbeg + kt * BK;
@@ -149,11 +110,11 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
           ma = &tmA2;
           mv = &tmV2;
         }
-        mbar_arrive_expect_tx(&full_bar[st], C::STAGE_BYTES);
-        tma_load_2d(sa, ma, k0, j0, &full_bar[st]);
-        tma_load_2d(sa + BM * 16, ma, k0 + 16, j0, &full_bar[st]);
-        tma_load_2d(sv, mv, k0, c0, &full_bar[st]);
-        tma_load_2d(sv + PT * 16, mv, k0 + 16, c0, &full_bar[st]);
+        bar_expect(&full_bar[st], C::STAGE_BYTES);
+        tma2d(sa, ma, k0, j0, &full_bar[st]);
+        tma2d(sa + BM * 16, ma, k0 + 16, j0, &full_bar[st]);
+        tma2d(sv, mv, k0, c0, &full_bar[st]);
+        tma2d(sv + PT * 16, mv, k0 + 16, c0, &full_bar[st]);
       }
     }
   } else {
@@ -164,8 +125,8 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
     const int vrow = wc * C::WN + q;  // + 8 cb
     for (int kt = 0; kt < nk; ++kt) {
       const int st = kt % C::STAGES;
-      mbar_wait(&full_bar[st], (kt / C::STAGES) & 1);
-      const uint32_t sa = smem_u32(smem) + st * C::STAGE_BYTES;
+      bar_wait(&full_bar[st], (kt / C::STAGES) & 1);
+      const uint32_t sa = su32(smem) + st * C::STAGE_BYTES;
       const uint32_t sv = sa + C::A_ELEMS * 8;
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
@@ -173,16 +134,16 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
         const uint32_t ba = sa + box * BM * 128, bv = sv + box * PT * 128;
         double af[C::JB], bf[C::CB];
 #pragma unroll
-        for (int jb = 0; jb < C::JB; ++jb) af[jb] = lds_sw(ba, arow + 8 * jb, col);
+        for (int jb = 0; jb < C::JB; ++jb) af[jb] = ldsw(ba, arow + 8 * jb, col);
 #pragma unroll
-        for (int cb = 0; cb < C::CB; ++cb) bf[cb] = lds_sw(bv, vrow + 8 * cb, col);
+        for (int cb = 0; cb < C::CB; ++cb) bf[cb] = ldsw(bv, vrow + 8 * cb, col);
 #pragma unroll
         for (int jb = 0; jb < C::JB; ++jb)
 #pragma unroll
           for (int cb = 0; cb < C::CB; ++cb) dmma_884(acc[jb][cb][0], acc[jb][cb][1], af[jb], bf[cb]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      if (lane == 0) bar_arrive(&empty_bar[st]);
     }
   }
   __syncthreads();  // ring drained: reuse it for the tile
@@ -252,37 +213,9 @@ cudaError_t symv_transpose(int k, int p, const double *V, int ldv, double *Vt, i
 }
 
 // ----------------------------------------------------------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void *f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(f);
-    else
-      cudaGetLastError();
-  }
-  return fn;
-}
-
 // 2D fp64 tensor map: rows x cols (cols contiguous, row pitch ld doubles), box [box_rows][16]
 static bool make_map(CUtensorMap *m, const double *base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tma_map_f64(m, base, rows, cols, ld, box_rows);
 }
 
 bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
@@ -290,7 +223,7 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
   if (mode2 == MODE2_PAIR && ((a.lda2 & 1) || ((uintptr_t)a.A2 & 15))) return false;
   if (epi != EPI_RAW && a.p > 64) return false;
   if ((a.lda & 1) || ((uintptr_t)a.A & 15)) return false;
-  return encode_fn() != nullptr;
+  return tma_encoder() != nullptr;
 }
 
 int symv_tma_rows() { return BM; }

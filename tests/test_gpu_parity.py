@@ -386,6 +386,22 @@ def test_solve_d10_against_oracle_and_brute_force(ctx, seed):
     assert len(tr) == info["outer_iters"]
 
 
+@pytest.mark.parametrize("d,seed", [(10, 0), (20, 1)])
+def test_solve_preconditioned_against_oracle(ctx, d, seed):
+    """Reading R35 (Gram-preconditioned truncated CG, precond_mu > 0): same certified optimum as
+    the oracle's preconditioned solve (residues recomputed by the oracle from the tuple)."""
+    Q, c = bqp_instance(d, seed)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 2, seed, precond_mu=0.05)
+    assert info["status"] == 0, info
+    amap, cnt, b = bqp.relax(Q, c)
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2, precond_mu=0.05), initial_factor(amap.shape[0], 2, seed))
+    assert o["status"] == "converged"
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+    X = ctx.solution(want_X=True)["X"]
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8
+
+
 def test_solve_toy_q2(ctx):
     info, sol, tr = _gpu_solve(ctx, np.array([[0.0, 1.0], [1.0, 0.0]]), np.zeros(2), 2, 0)
     assert info["status"] == 0 and abs(info["dual_obj"] + 2.0) <= 1e-6

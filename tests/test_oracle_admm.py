@@ -156,3 +156,27 @@ def test_lower_bound_property(d, seed):
     out = admm.solve(amap, cnt, b, None, prm, Y0)
     assert out["status"] == "converged"
     assert out["dual_obj"] <= bqp.brute_force(Q, c)[0] + 1e-6
+
+
+def test_preconditioned_tcg_operator_and_solve():
+    """Reading R35: the Gram preconditioner Prec(R) = P_Y(R W) is self-adjoint and positive
+    definite on the tangent space, reduces to W = I for an orthonormal-column Y at mu = 0 limit,
+    and the preconditioned RTR reaches the same certified optimum (eta_max <= 1e-8, objective
+    equal to the unpreconditioned solve's and below the brute-force minimum)."""
+    from oracle.rtr import gram_preconditioner
+
+    n, p = 30, 5
+    Y = random_unit_factor(n, p, 3)
+    P = gram_preconditioner(Y, 0.1)
+    U = sp.project(Y, random_matrix(n, p, 4))
+    V = sp.project(Y, random_matrix(n, p, 5))
+    assert abs(sp.inner(V, P(U)) - sp.inner(U, P(V))) <= 1e-12 * abs(sp.inner(V, P(U)))
+    assert sp.inner(U, P(U)) > 0 and np.abs(sp.rowdot(P(U), Y)).max() <= 1e-14
+    assert gram_preconditioner(Y, 0.0) is None
+    for seed in (0, 1):
+        Q, c, amap, cnt, b, prm, Y0 = _solve(10, seed, p0=2, precond_mu=0.05)
+        out = admm.solve(amap, cnt, b, None, prm, Y0)
+        ref = admm.solve(amap, cnt, b, None, admm.Params(p0=2), Y0)
+        assert out["status"] == "converged" and out["eta_max"] <= 1e-8
+        assert abs(out["dual_obj"] - ref["dual_obj"]) <= 1e-6 * (1 + abs(ref["dual_obj"]))
+        assert out["dual_obj"] <= bqp.brute_force(Q, c)[0] + 1e-6
