@@ -154,6 +154,64 @@ def oracle_sample(n, p, Mrows_fn, Y, U, rows_per_eval, budget_s=15.0):
                                  f"the n={n}, p={p} problem, cost+grad then HVP, {reps} reps; scaled by n/{rows_per_eval}")
 
 
+def cpu_model():
+    """Host CPU model name (lscpu / /proc/cpuinfo) for the oracle timings."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_full_eval(n, p, M, Y, U):
+    """One unsampled oracle evaluation pair (cost+grad, then HVP: oracle.subproblem.fixed_eval on the
+    whole n x n problem) on 1 core; returns seconds per evaluation."""
+    from oracle import subproblem as sp  # noqa: oracle is test infrastructure; cpu_baseline leg only
+
+    t0 = time.perf_counter()
+    sp.fixed_eval(M, Y)
+    sp.fixed_eval(M, Y, U)
+    return (time.perf_counter() - t0) / 2.0
+
+
+def oracle_solves(seeds=(0, 1, 2), d=10):
+    """The oracle's full Alg. 2 solves of BASELINE configs[0] (d = 10, 3 seeds) timed in-run on
+    1 core (plus the stored d = 40 oracle solve, tests/golden/oracle_solves.json, reported as cached)."""
+    from inputs import bqp_instance, initial_factor
+    from oracle import admm, bqp  # noqa: oracle is test infrastructure; cpu_baseline leg only
+
+    rows = []
+    for seed in seeds:
+        Q, c = bqp_instance(d, seed)
+        amap, cnt, b = bqp.relax(Q, c)
+        t0 = time.perf_counter()
+        o = admm.solve(amap, cnt, b, None, admm.Params(p0=2), initial_factor(amap.shape[0], 2, seed))
+        rows.append({"d": d, "seed": seed, "seconds": time.perf_counter() - t0, "status": o["status"],
+                     "outer_iters": o["outer_iters"], "dual_obj": o["dual_obj"], "eta_max": o["eta_max"],
+                     "cores": 1, "kind": "oracle, in-run"})
+    try:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_solves.json")))
+        for v in gold["solves"]:
+            if v.get("d") == 40:
+                rows.append({"d": 40, "seed": v.get("seed", 0), "seconds": v.get("seconds_1core"),
+                             "status": v.get("status"), "outer_iters": v.get("outer_iters"),
+                             "dual_obj": v.get("dual_obj"), "cores": 1,
+                             "kind": f"oracle, cached {gold.get('date')} at commit {gold.get('commit')} "
+                                     "(tests/golden/oracle_solves.json, tools/oracle_reference_solves.py)"})
+    except Exception:
+        pass
+    return rows
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -416,18 +474,22 @@ def run_gpu(args):
         from inputs import bqp_instance, initial_factor
 
         solves = []
-        for d in args.solve_d:
-            Q, c = bqp_instance(d, 0)
+        runs = [(d, 0) for d in args.solve_d]
+        if 10 in args.solve_d:  # configs[0] is quoted over 3 seeds (the oracle's in-run solves)
+            runs[runs.index((10, 0)) + 1:runs.index((10, 0)) + 1] = [(10, 1), (10, 2)]
+        for d, seed in runs:
+            kind = "er05" if d == 150 else "dense"  # configs[3] is the Erdos-Renyi sparse BQP
+            Q, c = bqp_instance(d, seed, kind)
             ctx.set_bqp(Q, c)
             nn = 1 + d + d * (d - 1) // 2
             p0 = 2 if d <= 10 else 4
-            ctx.set_params(ctx.default_params(p0=p0, time_limit_s=args.solve_time_limit))
-            ctx.set_initial_factor(initial_factor(nn, p0, 0))
+            ctx.set_params(ctx.default_params(p0=p0, time_limit_s=args.solve_time_limit, **args.solve_params))
+            ctx.set_initial_factor(initial_factor(nn, p0, seed))
             t0 = time.perf_counter()
             info = ctx.solve()
             wall = time.perf_counter() - t0
             paper = {10: 0.07, 20: 0.24, 30: 1.44, 40: 2.69, 50: 15.0, 60: 115.0, 70: 227.0, 80: 776.0}.get(d)
-            solves.append({"d": d, "n": nn, "seconds": wall, "paper_mean_seconds": paper,
+            solves.append({"d": d, "seed": seed, "kind": kind, "n": nn, "seconds": wall, "paper_mean_seconds": paper,
                            "paper_context": "ManiDSDP, MATLAB on an i9-10900 CPU, N(0,1) instances (P:789-798); "
                                             "context only, not the same instances",
                            "status": "converged" if info["status"] == 0 else
@@ -443,7 +505,18 @@ def run_gpu(args):
                                 Y, U, min(args.ref_rows, n), budget_s=args.ref_budget)
         del Mrows_src
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                               "host_cores": host_cores()}
+                               "host_cores": host_cores(), "cpu_model": cpu_model()}
+        if not args.no_full_oracle:
+            # one unsampled oracle evaluation at n = 16384 beside the sampled baseline
+            nf, pf = 16384, p
+            Mf = sweep_matrix_torch(nf, device=device).cpu().numpy()
+            Yf, Uf = sweep_factor(nf, pf)
+            sec = oracle_full_eval(nf, pf, Mf, Yf, Uf)
+            del Mf
+            out["cpu_baseline"]["full_eval_n16384"] = {
+                "seconds_per_eval": sec, "evals_per_s": 1.0 / sec, "n": nf, "p": pf, "cores": 1,
+                "sample": "oracle.subproblem.fixed_eval on the whole n = 16384 problem (cost+grad, then HVP)"}
+        out["oracle_solves"] = oracle_solves()
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -463,8 +536,12 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-oracle", action="store_true")
     ap.add_argument("--solve-d", type=lambda s: [int(x) for x in s.split(",") if x], default=[10, 40, 80])
     ap.add_argument("--solve-time-limit", type=float, default=120.0)
+    ap.add_argument("--solve-params", type=lambda s: {k: (float(v) if "." in v or "e" in v else int(v))
+                                                      for k, v in (a.split("=") for a in s.split(",") if a)},
+                    default={}, help="extra drsdp_params for the solves, e.g. precond_mu=0.01,eig_method=0")
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-budget", type=float, default=10.0)
     args = ap.parse_args()

@@ -124,10 +124,19 @@ typedef struct {
   int32_t stall_rtr;                   /* stagnation: stop RTR when ||grad|| has not halved within
                                           stall_rtr iterations and is within 100x of the inner
                                           tolerance (0 = never; reading R30)                       */
-  int32_t reserved;
+  int32_t eig_method;                  /* eigen step (eta_d, escape directions): 0 = auto (block
+                                          Lanczos for n >= 2048, dense dsyevd below), 1 = dense dsyevd
+                                          every outer iteration, 2 = block Lanczos always. With
+                                          Lanczos, convergence (eta_max <= tol) is confirmed by one dense
+                                          decomposition before the solve returns OK                    */
   double precond_mu;                   /* truncated-CG preconditioner Prec(R) = P_Y(R W),
                                           W = gbar (Y^T Y + mu gbar I)^{-1}, gbar = tr(Y^T Y)/p
                                           (reading R35); 0 = unpreconditioned                    */
+  int32_t lanczos_steps;               /* block-Lanczos steps per eigen step (block 16), 0 = 40   */
+  int32_t reserved;
+  double escape_gate;                  /* escape / rank change only when the inner solve ended with
+                                          ||grad|| <= escape_gate x its tolerance (reading R36);
+                                          0 = always                                               */
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);
@@ -184,6 +193,16 @@ int drsdp_get_trace(drsdp_ctx *ctx, int32_t max_rows, double *rows, int32_t *n_r
  * problem set by set_problem/set_bqp. */
 int drsdp_set_subproblem_matrix(drsdp_ctx *ctx, int64_t n, const double *M_dev, int64_t ldm);
 
+/* Row-block mode for the row-sharded evaluation (one block per GPU): register rows
+ * [row0, row1) of the n x n symmetric M (DEVICE, BORROWED as above, (row1 - row0) x ldm, ldm >= n
+ * even, 16-byte aligned). drsdp_subproblem_eval then takes the FULL n x p Y (and U), replicated
+ * on every block, and writes only the block's rows of egrad / rgrad / hvp ((row1 - row0) x p,
+ * pitch p); the cost it returns is the block's additive share -2 sum_{i in block} <(MY)_i, y_i>
+ * + ||M_block||_F^2 (+ ||Y^T Y||_F^2 on the block holding row 0), so the sum over the blocks of a
+ * partition is f. Needs p <= 64 and the TMA product kernel (else DRSDP_ERR_INVALID_ARG). */
+int drsdp_set_subproblem_rows(drsdp_ctx *ctx, int64_t n, int64_t row0, int64_t row1, const double *M_rows_dev,
+                              int64_t ldm);
+
 enum { DRSDP_EVAL_COSTGRAD = 1, DRSDP_EVAL_HVP = 2 };
 
 /* DEVICE pointers, caller-owned, asynchronous on the ctx stream (time with CUDA events on that
@@ -229,6 +248,17 @@ int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const doub
 int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev, int64_t ldt,
                    double sigma, const double *Y_dev, const double *U_dev, double *cost_dev,
                    double *egrad_dev, double *rgrad_dev, double *hvp_dev);
+
+/* Extreme eigenpairs of X = T - Diag(z) (Alg. 2 step 9 and eta_d) by block Lanczos
+ * with full re-orthogonalisation (block 16, at most `steps` blocks, basis capped at n): the
+ * partial eigendecomposition P:342 allows. DEVICE inputs T (n x ldt, symmetric) and z (n) for
+ * the current problem's n; V_dev (DEVICE, caller-owned, n*nvec row-major) receives the Ritz
+ * vectors of the nvec smallest Ritz values; HOST outputs ritz (nvec ascending Ritz values, NaN past
+ * the basis size), resid (their residual norms ||X v - theta v||, may be NULL), lam_max (largest
+ * Ritz value, may be NULL) and basis (basis size, may be NULL). Ritz values bound the extreme
+ * eigenvalues from inside the spectrum. Synchronous. */
+int drsdp_x_eigs(drsdp_ctx *ctx, const double *T_dev, int64_t ldt, const double *z_dev, int32_t steps, int32_t nvec,
+                 double *ritz, double *lam_max, double *V_dev, double *resid, int32_t *basis);
 
 /* Device kernel launches issued by this context since creation (for launch accounting). */
 int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count);

@@ -55,6 +55,8 @@ class Params:
         self.stall_rtr = 10
         self.max_tcg = 100
         self.precond_mu = 0.0  # reading R35: Gram right-preconditioner of the truncated CG (0 = off)
+        self.escape_gate = 0.0  # reading R36: escape / rank change only after an inner solve within
+                                # escape_gate x its tolerance (0 = always)
         for k, v in kw.items():
             if not hasattr(self, k):
                 raise TypeError(f"unknown parameter {k}")
@@ -192,10 +194,15 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         Vs = escape_directions(res["lam"], res["V"], prm.eig_neg_tol, prm.escape_max)
         if Vs is not None and Y.shape[1] + Vs.shape[1] > n:  # p never exceeds n (S has rank <= n)
             Vs = Vs[:, : n - Y.shape[1]] if Y.shape[1] < n else None
+        # escape gate (reading R36): X^{k+1} certifies the subproblem (Prop 4.3) only at a
+        # stationary point; an inner solve far above its tolerance keeps the rank unchanged
+        gated = prm.escape_gate > 0 and info["gnorm"] > prm.escape_gate * grad_tol
+        if gated:
+            Vs = None
         # rank tolerance tied to the residual (reading R32); no reduction in an iteration that
         # escapes (reading R34: the escape columns of the previous iteration are O(sqrt(|lambda|/sigma))
         # and a relative tolerance would remove them before they grow)
-        if Vs is None:
+        if Vs is None and not gated:
             Y = rank_reduce(Y, min(prm.rank_tol, max(1e-8, 0.01 * math.sqrt(res["eta_max"]))))
         if Vs is not None:
             delta = Vs.shape[1]

@@ -22,9 +22,9 @@ TRACE_COLUMNS = ("iter", "eta_p", "eta_d", "eta_g", "eta_max", "primal_obj", "du
 EXPORTED = ("drsdp_create", "drsdp_destroy", "drsdp_last_error", "drsdp_sync", "drsdp_set_problem",
             "drsdp_set_bqp", "drsdp_get_sizes", "drsdp_export_index_map", "drsdp_default_params",
             "drsdp_set_params", "drsdp_set_initial_factor", "drsdp_solve", "drsdp_get_solution",
-            "drsdp_get_trace", "drsdp_set_subproblem_matrix", "drsdp_subproblem_eval",
+            "drsdp_get_trace", "drsdp_set_subproblem_matrix", "drsdp_set_subproblem_rows", "drsdp_subproblem_eval",
             "drsdp_subproblem_eval_host", "drsdp_assemble_M", "drsdp_y_update", "drsdp_dual_update",
-            "drsdp_alm_eval", "drsdp_launch_count", "drsdp_profile_enable", "drsdp_profile_read")
+            "drsdp_alm_eval", "drsdp_x_eigs", "drsdp_launch_count", "drsdp_profile_enable", "drsdp_profile_read")
 
 
 class DrsdpError(RuntimeError):
@@ -40,7 +40,9 @@ class Params(C.Structure):
                 ("eps_floor", C.c_double), ("time_limit_s", C.c_double), ("p0", C.c_int32),
                 ("max_outer", C.c_int32), ("max_rtr", C.c_int32), ("max_tcg", C.c_int32),
                 ("escape_max", C.c_int32), ("mode", C.c_int32), ("seed", C.c_uint64), ("rho_reg", C.c_double),
-                ("stall_rtr", C.c_int32), ("reserved", C.c_int32), ("precond_mu", C.c_double)]
+                ("stall_rtr", C.c_int32), ("eig_method", C.c_int32), ("precond_mu", C.c_double),
+                ("lanczos_steps", C.c_int32), ("reserved", C.c_int32),
+                ("escape_gate", C.c_double)]
 
 
 class Info(C.Structure):
@@ -84,12 +86,15 @@ def load_library():
         "drsdp_get_solution": (C.c_int, [vp, dp, dp, C.POINTER(i32), dp, dp]),
         "drsdp_get_trace": (C.c_int, [vp, i32, dp, C.POINTER(i32)]),
         "drsdp_set_subproblem_matrix": (C.c_int, [vp, i64, dp, i64]),
+        "drsdp_set_subproblem_rows": (C.c_int, [vp, i64, i64, i64, dp, i64]),
         "drsdp_subproblem_eval": (C.c_int, [vp, i32, i32, dp, dp, dp, dp, dp, dp]),
         "drsdp_subproblem_eval_host": (C.c_int, [vp, i32, i32, dp, dp, dp, dp, dp, dp]),
         "drsdp_assemble_M": (C.c_int, [vp, dp, dp, i64, C.c_double, dp, i64]),
         "drsdp_y_update": (C.c_int, [vp, i32, dp, dp]),
         "drsdp_dual_update": (C.c_int, [vp, i32, dp, dp, C.c_double, dp, i64, dp, dp]),
         "drsdp_alm_eval": (C.c_int, [vp, i32, i32, dp, i64, C.c_double, dp, dp, dp, dp, dp, dp]),
+        "drsdp_x_eigs": (C.c_int, [vp, dp, i64, dp, i32, i32, dp, C.POINTER(C.c_double), dp, dp,
+                                   C.POINTER(i32)]),
         "drsdp_launch_count": (C.c_int, [vp, C.POINTER(i64)]),
         "drsdp_profile_enable": (C.c_int, [vp, C.c_int]),
         "drsdp_profile_read": (C.c_int, [vp, i32, C.POINTER(C.c_double), C.POINTER(i64)]),
@@ -228,6 +233,11 @@ class Context:
         self._keep = [M_dev]
         return self._check(self.lib.drsdp_set_subproblem_matrix(self.h, n, _ptr(M_dev), ldm))
 
+    def set_subproblem_rows(self, n, row0, row1, M_rows_dev, ldm):
+        """Row-block mode (row-sharded evaluation): rows [row0, row1) of the n x n matrix."""
+        self._keep = [M_rows_dev]
+        return self._check(self.lib.drsdp_set_subproblem_rows(self.h, n, row0, row1, _ptr(M_rows_dev), ldm))
+
     def subproblem_eval(self, flags, p, Y, U=None, cost=None, egrad=None, rgrad=None, hvp=None):
         return self._check(self.lib.drsdp_subproblem_eval(self.h, flags, p, _ptr(Y), _ptr(U), _ptr(cost),
                                                           _ptr(egrad), _ptr(rgrad), _ptr(hvp)))
@@ -253,6 +263,17 @@ class Context:
 
     def y_update(self, p, Y, y):
         return self._check(self.lib.drsdp_y_update(self.h, p, _ptr(Y), _ptr(y)))
+
+    def x_eigs(self, T, ldt, z, steps, nvec, V):
+        """Block-Lanczos extreme eigenpairs of X = T - Diag(z) (device T, z, V): returns
+        (ritz values (nvec), residual norms (nvec), largest Ritz value, basis size)."""
+        ritz = np.empty(max(nvec, 1))
+        resid = np.empty(max(nvec, 1))
+        lmax = C.c_double()
+        basis = C.c_int32()
+        self._check(self.lib.drsdp_x_eigs(self.h, _ptr(T), ldt, _ptr(z), steps, nvec, ritz.ctypes.data,
+                                          C.byref(lmax), _ptr(V), resid.ctypes.data, C.byref(basis)))
+        return ritz[:nvec], resid[:nvec], lmax.value, basis.value
 
     def dual_update(self, p, Y, y, sigma, T, ldt, z, scalars):
         return self._check(self.lib.drsdp_dual_update(self.h, p, _ptr(Y), _ptr(y), sigma, _ptr(T), ldt, _ptr(z),

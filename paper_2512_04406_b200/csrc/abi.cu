@@ -83,6 +83,9 @@ int ensure_workspace(drsdp_ctx *ctx, int64_t n, int p) {
 // workspace / tile counters on demand and records the live timing events (kind 1..3) if enabled.
 int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int prof_kind) {
   static const bool no_tma = std::getenv("DRSDP_NO_TMA") != nullptr;
+  if (a.ncols > 0 && a.ncols != a.n && (no_tma || !symv_tma_supported(a, epi, mode2, atr)))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG,
+                     "row-block product needs the TMA kernel (even pitch, 16 B aligned rows, p <= 64)");
   // (small n keeps the register-direct gather kernel: one launch instead of assembly + product)
   if (!no_tma && mode2 == MODE2_GATHER && !atr && a.n >= 2048 && (a.lda % 2) == 0 && ((uintptr_t)a.A & 15) == 0 &&
       (a.k == 0 || a.k == a.n)) {
@@ -133,7 +136,8 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
   if (!no_tma && symv_tma_supported(a, epi, mode2, atr)) {
     const int pt = symv_pt(a.p), bm = symv_tma_rows(), bk = symv_tma_kstep();
     const bool pair = mode2 == MODE2_PAIR;
-    const int ktot = pair ? 2 * ((a.n + bk - 1) / bk * bk) : a.n;
+    const int kn = a.ncols > 0 ? a.ncols : a.n;
+    const int ktot = pair ? 2 * ((kn + bk - 1) / bk * bk) : kn;
     const int ntiles = ((a.n + bm - 1) / bm) * symv_chunks(a.p, epi);
     // split-K: one CTA per SM (the ring uses most of shared memory); waves x k-rows cost model
     int S = 1;
@@ -153,7 +157,7 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bm * pt), "alloc split workspace");
     CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
     CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
-    const int64_t ldvt = (a.n + 1) / 2 * 2;
+    const int64_t ldvt = (kn + 1) / 2 * 2;
     CK(ctx->vt_buf.ensure((size_t)(pair ? 2 : 1) * a.p * ldvt), "alloc V^T");
     if (!pair) a.A2 = nullptr;
     a.part = ctx->symv_part.ptr;
@@ -412,6 +416,8 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
                double *rho, const double *cost_extra_dev, bool have_gram) {
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
+  if (p > 64 && ctx->sub_rows_mode && M == ctx->sub_M)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "row-block evaluation supports p <= 64");
   if (p > 64) {
     if (flags & DRSDP_EVAL_COSTGRAD) {
       rc = gram_generic(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
@@ -428,13 +434,19 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
     }
     return DRSDP_OK;
   }
+  // row-block mode (drsdp_set_subproblem_rows): M holds rows [r0, r0 + nloc) of the n x n matrix;
+  // G, K come from the full (replicated) Y, U; the epilogue works on the block's rows
+  const bool rows = ctx->sub_rows_mode && M == ctx->sub_M;
+  const int r0 = rows ? (int)ctx->sub_row0 : 0;
+  const int nloc = rows ? (int)ctx->sub_nloc : n;
   if (flags & DRSDP_EVAL_COSTGRAD) {
     rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
     if (rc) return rc;
-    SymvArgs a = base_symv(ctx, n, p, M, ldm);
+    SymvArgs a = base_symv(ctx, nloc, p, M, ldm);
+    if (rows) a.ncols = n;
     a.V = Y;
     a.ldv = ldv;
-    a.Y = Y;
+    a.Y = Y + (size_t)r0 * ldv;
     a.ldy = ldv;
     a.G = G;
     a.out = rgrad;
@@ -443,7 +455,8 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
     a.lde = ldv;
     a.rho_out = rho;
     a.scal_out = ctx->d_scal + S_SCAL;
-    a.gg = ctx->d_scal + S_GG;
+    // row blocks: the cost is additive over blocks with ||G||^2 counted by the block holding row 0
+    a.gg = (rows && r0 > 0) ? ctx->d_scal + S_ZERO : ctx->d_scal + S_GG;
     a.cost_extra = cost_extra_dev;
     a.cost_out = cost ? cost : ctx->d_scal + S_COST;
     rc = run_symv(ctx, a, EPI_COSTGRAD, false);
@@ -452,12 +465,13 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
   if (flags & DRSDP_EVAL_HVP) {
     rc = gram(ctx, n, p, Y, ldv, U, G, K, ctx->d_scal + S_GG);
     if (rc) return rc;
-    SymvArgs a = base_symv(ctx, n, p, M, ldm);
+    SymvArgs a = base_symv(ctx, nloc, p, M, ldm);
+    if (rows) a.ncols = n;
     a.V = U;
     a.ldv = ldv;
-    a.Y = Y;
+    a.Y = Y + (size_t)r0 * ldv;
     a.ldy = ldv;
-    a.U = U;
+    a.U = U + (size_t)r0 * ldv;
     a.ldu = ldv;
     a.G = G;
     a.K = K;
@@ -1044,6 +1058,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->rho_reg = 1e3;
   o->stall_rtr = 10;
   o->precond_mu = 0.0;
+  o->escape_gate = 0.0;
   return DRSDP_OK;
 }
 
@@ -1053,7 +1068,8 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
-        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.precond_mu >= 0))
+        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.precond_mu >= 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
+        q.escape_gate >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;
   return DRSDP_OK;
@@ -1086,6 +1102,9 @@ int drsdp_set_subproblem_matrix(drsdp_ctx *ctx, int64_t n, const double *M_dev, 
   ctx->sub_M = M_dev;
   ctx->sub_n = n;
   ctx->sub_ldm = ldm;
+  ctx->sub_rows_mode = false;
+  ctx->sub_row0 = 0;
+  ctx->sub_nloc = n;
   ctx->sub_cached_valid = false;
   CK(ctx->sub_rho.ensure(n), "alloc rho");
   int rc = ensure_red(ctx, 1184, 2);
@@ -1095,6 +1114,36 @@ int drsdp_set_subproblem_matrix(drsdp_ctx *ctx, int64_t n, const double *M_dev, 
   // cost extra = [||M||^2, 0]
   KL(combine_launch(ctx->d_scal + S_MM, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA, ctx->stream), "combine");
   KL(combine_launch(nullptr, 0.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA + 1, ctx->stream), "combine");
+  return DRSDP_OK;
+}
+
+int drsdp_set_subproblem_rows(drsdp_ctx *ctx, int64_t n, int64_t row0, int64_t row1, const double *M_rows_dev,
+                              int64_t ldm) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (n <= 0 || n > (1 << 30) || row0 < 0 || row1 <= row0 || row1 > n || !M_rows_dev || ldm < n || (ldm & 1) ||
+      ((uintptr_t)M_rows_dev & 15))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG,
+                     "set_subproblem_rows: need 0 <= row0 < row1 <= n, ldm >= n even, 16 B aligned rows");
+  cudaSetDevice(ctx->device);
+  const int64_t nloc = row1 - row0;
+  ctx->sub_M = M_rows_dev;
+  ctx->sub_n = n;
+  ctx->sub_ldm = ldm;
+  ctx->sub_rows_mode = true;
+  ctx->sub_row0 = row0;
+  ctx->sub_nloc = nloc;
+  ctx->sub_cached_valid = false;
+  CK(ctx->sub_rho.ensure(n), "alloc rho");
+  int rc = ensure_red(ctx, 1184, 2);
+  if (rc) return rc;
+  // ||M_rows||_F^2 over the block (nloc rows of n columns): the block's share of the cost constant
+  KL(fro2_rows_launch(nloc, n, M_rows_dev, ldm, ctx->red_part.ptr, ctx->counters + C_FRO, ctx->d_scal + S_MM,
+                      ctx->stream),
+     "fro2");
+  KL(combine_launch(ctx->d_scal + S_MM, 1.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA, ctx->stream), "combine");
+  KL(combine_launch(nullptr, 0.0, nullptr, 0.0, 0.0, ctx->d_scal + S_EXTRA + 1, ctx->stream), "combine");
+  KL(combine_launch(nullptr, 0.0, nullptr, 0.0, 0.0, ctx->d_scal + S_ZERO, ctx->stream), "combine");
   return DRSDP_OK;
 }
 

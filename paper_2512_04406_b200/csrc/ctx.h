@@ -65,6 +65,7 @@ enum Slot {
   S_YCA = 24,      // 2: yS . cA
   S_ALM = 26,      // 3: ALM assembly sums [sum R^2, <T, S+C>, ||T||^2]
   S_FLAG = 30,     // retraction flag (int stored in a double slot)
+  S_ZERO = 31,     // constant 0 (row-block cost: ||G||^2 counted once)
   S_TOTAL = 64
 };
 
@@ -144,6 +145,8 @@ struct drsdp_ctx {
   // fixed-M subproblem (borrowed)
   const double *sub_M = nullptr;
   int64_t sub_n = 0, sub_ldm = 0;
+  bool sub_rows_mode = false;  // drsdp_set_subproblem_rows: sub_M holds rows [sub_row0, + sub_nloc)
+  int64_t sub_row0 = 0, sub_nloc = 0;
   drsdp::DBuf<double> sub_G, sub_K, sub_rho;  // fixed-M eval cache (drsdp_subproblem_eval only)
   drsdp::DBuf<double> g_scratch;              // G recomputed as a by-product of K inside HVPs
   const double *sub_cached_Y = nullptr;

@@ -570,14 +570,14 @@ __global__ void __launch_bounds__(256) init_d_kernel(int n, const int32_t *amap,
   }
 }
 
-// ||M||_F^2 over an n x n matrix with pitch ld
-__global__ void __launch_bounds__(256) fro2_kernel(int n, const double *M, int64_t ld, double *part,
+// ||M||_F^2 over a rows x cols matrix with pitch ld
+__global__ void __launch_bounds__(256) fro2_kernel(int64_t rows, int cols, const double *M, int64_t ld, double *part,
                                                    unsigned *counter, double *out) {
   __shared__ double scratch[8];
   double v[1] = {0.0};
-  const int64_t total = (int64_t)n * n;
+  const int64_t total = rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n, j = e - i * n;
+    const int64_t i = e / cols, j = e - i * cols;
     const double x = __ldcs(M + i * ld + j);
     v[0] = fma(x, x, v[0]);
   }
@@ -948,7 +948,12 @@ cudaError_t init_d_launch(int n, const int32_t *amap, int64_t ldmap, const doubl
 }
 cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsigned *counter, double *out,
                         cudaStream_t st) {
-  fro2_kernel<<<1184, 256, 0, st>>>(n, M, ld, part, counter, out);
+  fro2_kernel<<<1184, 256, 0, st>>>(n, n, M, ld, part, counter, out);
+  return cudaGetLastError();
+}
+cudaError_t fro2_rows_launch(int64_t rows, int64_t cols, const double *M, int64_t ld, double *part, unsigned *counter,
+                             double *out, cudaStream_t st) {
+  fro2_kernel<<<1184, 256, 0, st>>>(rows, (int)cols, M, ld, part, counter, out);
   return cudaGetLastError();
 }
 cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,

@@ -102,6 +102,8 @@ cudaError_t vdot_launch(int64_t len, const double *a, const double *b, double *p
                         double *out, cudaStream_t st);
 cudaError_t init_d_launch(int n, const int32_t *amap, int64_t ldmap, const double *b, const int32_t *cnt,
                           double *T, int64_t ldt, cudaStream_t st);
+cudaError_t fro2_rows_launch(int64_t rows, int64_t cols, const double *M, int64_t ld, double *part, unsigned *counter,
+                             double *out, cudaStream_t st);
 cudaError_t fro2_launch(int n, const double *M, int64_t ld, double *part, unsigned *counter, double *out,
                         cudaStream_t st);
 cudaError_t combine_launch(const double *a, double s0, const double *b, double s1, double c, double *out,

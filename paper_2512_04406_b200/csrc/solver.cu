@@ -19,6 +19,7 @@
 
 #include "ctx.h"
 #include "kernels.cuh"
+#include "lanczos.cuh"
 #include "symv.cuh"
 
 namespace drsdp {
@@ -53,6 +54,7 @@ struct SolverState {
   DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
   DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
   DBuf<double> Apre, Wpre, pwork;  // tCG preconditioner (reading R35): A = G/gbar + mu I, W = A^{-1}
+  LanczosWork lz;                  // block Lanczos eigen step (lanczos.cu)
   DBuf<int> devinfo;
   DBuf<double> work, gwork;
   DBuf<TcgDev> tcg;              // device-resident tCG scalars
@@ -92,6 +94,7 @@ void free_solver(drsdp_ctx *ctx) {
                         &s->work, &s->Geig, &s->Gw, &s->gwork, &s->Apre, &s->Wpre, &s->pwork};
   for (auto *b : bs) b->release();
   s->devinfo.release();
+  s->lz.release();
   s->tcg.release();
   if (s->h_tcg) cudaFreeHost(s->h_tcg);
   for (auto &g : s->graphs)
@@ -113,7 +116,7 @@ struct Run {
   const drsdp_params &prm;
   int n;
   double sigma = 1.0;
-  int64_t costgrad = 0, hvp = 0, rtr_total = 0, tcg_total = 0;
+  int64_t costgrad = 0, hvp = 0, rtr_total = 0, tcg_total = 0, lz_steps = 0;
 
   int costgrad_at(Point &P, int p) {
     ++costgrad;
@@ -703,42 +706,81 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     KL(vdot_launch(P.m, s->ystar.ptr, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY,
                    ctx->stream),
        "vdot");
-    // X = T - Diag(z) and its eigen-decomposition
-    KL(make_x_launch(n, s->T.ptr, P.ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
-    {
-      int lwork = (int)s->work.cap - 1;
-      if (cusolverDnDsyevd(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, s->X.ptr, n, s->W.ptr,
-                           s->work.ptr, lwork, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
-        return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd");
-      ctx->launches++;
-    }
-    CK(cudaMemcpyAsync(lam.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
-    int eig_info = 0;
-    CK(cudaMemcpyAsync(&eig_info, s->devinfo.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read info");
+    // X = T - Diag(z) and its extreme eigenpairs: block Lanczos on
+    // T V - z o V (partial decomposition) or the dense dsyevd; eta_max <= tol reported by
+    // Lanczos is confirmed by one dense decomposition (the certificate never rests on Ritz values)
     RC(read_scalars(ctx, S_DUAL, 8));
-    if (eig_info != 0)
-      return set_error(ctx, DRSDP_ERR_NUMERIC, "eigen-decomposition of X failed (dsyevd info " + std::to_string(eig_info) + ")");
     const double R_norm = std::sqrt(std::max(0.0, ctx->h_scal[S_DUAL]));
     const double CT = ctx->h_scal[S_DUAL + 2];
     const double zsum = ctx->h_scal[S_ZSUM];
     dobj = ctx->h_scal[S_BY];
     pobj = CT + zsum;
     eta_p = R_norm / (1.0 + C_norm);
-    eta_d = std::max(0.0, -lam[0]) / (1.0 + std::fabs(lam[n - 1]));
     eta_g = std::fabs(dobj - pobj) / (1.0 + std::fabs(dobj) + std::fabs(pobj));
+    const bool lanczos = prm.eig_method == 2 || (prm.eig_method == 0 && n >= 2048);
+    const int nvec = std::max(1, std::min(prm.escape_max, n));
+    int nlam = 0;                   // smallest eigen/Ritz values available in lam[0..nlam)
+    double lam_top = 0.0;           // largest eigen/Ritz value
+    const double *vec_cols = nullptr;  // escape candidates, column-major (column c at vec_cols + c n)
+    bool dense_done = false;
+    auto dense_eig = [&]() -> int {
+      KL(make_x_launch(n, s->T.ptr, P.ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
+      int lwork = (int)s->work.cap - 1;
+      if (cusolverDnDsyevd(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, s->X.ptr, n, s->W.ptr,
+                           s->work.ptr, lwork, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
+        return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnDsyevd");
+      ctx->launches++;
+      CK(cudaMemcpyAsync(lam.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
+      int eig_info = 0;
+      CK(cudaMemcpyAsync(&eig_info, s->devinfo.ptr, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "read info");
+      CK(cudaStreamSynchronize(ctx->stream), "sync");
+      if (eig_info != 0)
+        return set_error(ctx, DRSDP_ERR_NUMERIC,
+                         "eigen-decomposition of X failed (dsyevd info " + std::to_string(eig_info) + ")");
+      nlam = n;
+      lam_top = lam[n - 1];
+      vec_cols = s->X.ptr;
+      dense_done = true;
+      return DRSDP_OK;
+    };
+    if (lanczos) {
+      const int b = std::min(16, n);
+      const int kmax = std::max(1, std::min(prm.lanczos_steps > 0 ? prm.lanczos_steps : 40, n / b));
+      if (s->lz.n != n || s->lz.b != b || s->lz.kmax != kmax) {
+        const int e = s->lz.ensure(n, b, kmax);
+        if (e) RC(cuda_check(ctx, (cudaError_t)e, "alloc lanczos"));
+      }
+      LanczosResult lr;
+      RC(lanczos_extreme(ctx, s->lz, s->sol, s->T.ptr, P.ld, s->z.ptr, nvec, prm.seed * 7919ull + (uint64_t)k, lr));
+      nlam = std::min((int)lr.theta.size(), n);
+      for (int i = 0; i < nlam; ++i) lam[i] = lr.theta[i];
+      lam_top = lr.lam_max;
+      run.lz_steps += lr.steps;
+      // Ritz vectors of the nvec smallest Ritz values, transposed to column-major
+      KL(symv_transpose(n, std::min(nvec, lr.basis), s->lz.V.ptr, std::min(nvec, lr.basis), s->Vst.ptr, n, nullptr,
+                        ctx->stream),
+         "transpose Ritz vectors");
+      vec_cols = s->Vst.ptr;
+      const double ed = std::max(0.0, -lam[0]) / (1.0 + std::fabs(lam_top));
+      if (std::max(eta_p, std::max(ed, eta_g)) <= prm.tol) RC(dense_eig());  // confirm
+    } else {
+      RC(dense_eig());
+    }
+    eta_d = std::max(0.0, -lam[0]) / (1.0 + std::fabs(lam_top));
     const double eta_max = std::max(eta_p, std::max(eta_d, eta_g));
     double row[13] = {(double)(k + 1), eta_p, eta_d, eta_g, eta_max, pobj, dobj, run.sigma, (double)p,
                       (double)rtr_it, (double)tcg_it, 0.0, 0.0};
     if (verbose) {
       int nneg = 0;
-      const double th = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
-      while (nneg < n && lam[nneg] < th) ++nneg;
+      const double th = -prm.eig_neg_tol * (1.0 + std::fabs(lam_top));
+      while (nneg < nlam && lam[nneg] < th) ++nneg;
       std::fprintf(stderr,
                    "[drsdp] k=%d p=%d sigma=%.3e eta_p=%.3e eta_d=%.3e eta_g=%.3e dobj=%.12f rtr=%d tcg=%d exit=%s "
-                   "gn0=%.2e gn=%.2e tol=%.2e warm_t=%.2g neg=%d lmin=%.3e lmax=%.3e t=%.2fs\n",
+                   "gn0=%.2e gn=%.2e tol=%.2e warm_t=%.2g neg=%d%s lmin=%.3e lmax=%.3e t=%.2fs\n",
                    k + 1, p, run.sigma, eta_p, eta_d, eta_g, dobj, rtr_it, tcg_it,
                    run.last_exit == 0 ? "tol" : run.last_exit == 1 ? "stall" : run.last_exit == 2 ? "maxit" : "radius",
-                   run.last_gn0, s->cur.gn, grad_tol, run.last_warm_t, nneg, lam[0], lam[n - 1], now_s() - t0);
+                   run.last_gn0, s->cur.gn, grad_tol, run.last_warm_t, nneg, dense_done ? "" : "(ritz)", lam[0],
+                   lam_top, now_s() - t0);
     }
     if (eta_max <= prm.tol) {
       status = DRSDP_OK;
@@ -746,16 +788,21 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       ctx->trace.insert(ctx->trace.end(), row, row + 13);
       break;
     }
-    // escape directions: eigenvectors with lambda < -eig_neg_tol (1 + |lambda_max|)
-    const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam[n - 1]));
+    // escape directions: eigenvectors (Ritz vectors) with lambda < -eig_neg_tol (1 + |lambda_max|)
+    const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam_top));
     int dv = 0;
-    while (dv < prm.escape_max && dv < n && lam[dv] < thresh) ++dv;
+    while (dv < prm.escape_max && dv < nlam && dv < (dense_done ? n : nvec) && lam[dv] < thresh) ++dv;
     if (dv > 0 && p + dv > std::min(DRSDP_MAX_P, n)) dv = std::max(0, std::min(DRSDP_MAX_P, n) - p);
+    // escape gate (reading R36): the certificate X^{k+1} is the subproblem's (Prop 4.3) only at a
+    // stationary point; while the inner solve ends far above its tolerance, keep the rank (no escape,
+    // no reduction)
+    const bool gated = prm.escape_gate > 0.0 && s->cur.gn > prm.escape_gate * grad_tol;
+    if (gated) dv = 0;
     // rank reduction (readings R15, R32, R34): only in an iteration that does not escape, compress
     // Y to its numerical rank at the tolerance rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta_max))).
     // Eigenpairs of the p x p Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so
     // row/column-major agree).
-    if (dv == 0) {
+    if (dv == 0 && !gated) {
       CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
          "copy G");
       const int lw = (int)s->gwork.cap - 1;
@@ -794,7 +841,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       if (p + dv > s->ldp) RC(set_pitch(ctx, ((p + dv + 63) / 64) * 64, true, p));
       // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]
       std::vector<double> Vh((size_t)n * dv);
-      CK(cudaMemcpyAsync(Vh.data(), s->X.ptr, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
+      CK(cudaMemcpyAsync(Vh.data(), vec_cols, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
          "read V");
       CK(cudaStreamSynchronize(ctx->stream), "sync");
       for (int c = 0; c < dv; ++c) {

@@ -19,6 +19,10 @@ struct SymvArgs {
   const double *A = nullptr;
   int64_t lda = 0;
   int n = 0, p = 0, k = 0;
+  // row-block mode of the TMA kernel (row-sharded evaluation): A holds n rows of a
+  // symmetric ncols x ncols matrix (output rows), contracted against all ncols rows of V; the
+  // epilogue operands (Y, U, rho, outputs) are then the block's own n rows. 0 = square (ncols = n).
+  int ncols = 0;
   const int *skip = nullptr;  // device flag: when non-zero at launch time the kernel does nothing
   // MODE2_PAIR: second operand pair, same access pattern as (A, V)
   const double *A2 = nullptr;

@@ -74,8 +74,9 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
   const int tile = blockIdx.x + gridDim.x * blockIdx.z;
   const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;
   const int j0 = blockIdx.x * BM;
-  const int kpad = (n + BK - 1) / BK * BK;
-  const int ktot = PAIR ? 2 * kpad : n;
+  const int kn = a.ncols > 0 ? a.ncols : n;  // contraction length (row-block mode: all columns)
+  const int kpad = (kn + BK - 1) / BK * BK;
+  const int ktot = PAIR ? 2 * kpad : kn;
   const int kbeg = split * a.rows_per_split;
   const int kend = min(ktot, kbeg + a.rows_per_split);
   const int nk = (kend - kbeg + BK - 1) / BK;
@@ -219,7 +220,9 @@ static bool make_map(CUtensorMap *m, const double *base, int64_t rows, int64_t c
 }
 
 bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
-  if (mode2 == MODE2_GATHER || atr || (a.k > 0 && a.k != a.n)) return false;
+  // symmetric n x n operands only (k = 0): with an explicit k the operand is a general k x n matrix
+  // whose product is A^T V, while this kernel streams rows of A (A V)
+  if (mode2 == MODE2_GATHER || atr || a.k > 0) return false;
   if (mode2 == MODE2_PAIR && ((a.lda2 & 1) || ((uintptr_t)a.A2 & 15))) return false;
   if (epi != EPI_RAW && a.p > 64) return false;
   if ((a.lda & 1) || ((uintptr_t)a.A & 15)) return false;
@@ -262,25 +265,27 @@ static cudaError_t tma_dispatch(const SymvArgs &a, int epi, bool pair, const CUt
   }
 }
 
-// Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR), ldvt = round_up(n, 2)
+// Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR), ldvt = round_up(kn, 2), kn =
+// the contraction length (ncols in row-block mode, else n)
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st) {
   const int pt = symv_pt(a.p);
   const bool pair = a.A2 != nullptr;
-  dim3 tg((a.n + 31) / 32, (a.p + 31) / 32);
-  transpose_kernel<<<tg, 256, 0, st>>>(a.n, a.p, a.V, a.ldv, Vt, ldvt, a.skip);
+  const int kn = a.ncols > 0 ? a.ncols : a.n;
+  dim3 tg((kn + 31) / 32, (a.p + 31) / 32);
+  transpose_kernel<<<tg, 256, 0, st>>>(kn, a.p, a.V, a.ldv, Vt, ldvt, a.skip);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   double *Vt2 = Vt + (size_t)a.p * ldvt;
   if (pair) {
-    transpose_kernel<<<tg, 256, 0, st>>>(a.n, a.p, a.V2, a.ldv2, Vt2, ldvt, a.skip);
+    transpose_kernel<<<tg, 256, 0, st>>>(kn, a.p, a.V2, a.ldv2, Vt2, ldvt, a.skip);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   CUtensorMap m[4];
-  if (!make_map(&m[0], a.A, a.n, a.n, a.lda, BM) || !make_map(&m[1], Vt, a.p, a.n, ldvt, pt))
+  if (!make_map(&m[0], a.A, a.n, kn, a.lda, BM) || !make_map(&m[1], Vt, a.p, kn, ldvt, pt))
     return cudaErrorInvalidValue;
   if (pair) {
-    if (!make_map(&m[2], a.A2, a.n, a.n, a.lda2, BM) || !make_map(&m[3], Vt2, a.p, a.n, ldvt, pt))
+    if (!make_map(&m[2], a.A2, a.n, kn, a.lda2, BM) || !make_map(&m[3], Vt2, a.p, kn, ldvt, pt))
       return cudaErrorInvalidValue;
   } else {
     m[2] = m[0];

@@ -223,6 +223,96 @@ def test_index_map_bit_exact(ctx, d):
     assert np.array_equal(seg_ptr, np.concatenate([[0], np.cumsum(np.bincount(ids, minlength=m))]))
 
 
+_KEYS = {}
+
+
+def _graded_lex_keys(d):
+    """Sorted integer keys of all square-free monomials of degree <= 4 (see below)."""
+    if d not in _KEYS:
+        D = d + 1
+        keys = [np.zeros(1, np.int64)]
+        for k in range(1, 5):
+            # sorted k-subsets of range(d) as rows of a k-column array (vectorised combinations)
+            t = np.arange(d, dtype=np.int64)[:, None]
+            for _ in range(k - 1):
+                last = t[:, -1]
+                reps = d - 1 - last
+                base = np.repeat(t, reps, axis=0)
+                nxt = np.concatenate([np.arange(l + 1, d) for l in last]) if t.shape[0] else np.zeros(0, np.int64)
+                t = np.hstack([base, nxt[:, None]])
+            kk = np.full(t.shape[0], k * D ** 4, np.int64)
+            for c in range(k):
+                kk += (t[:, c] + 1) * D ** (3 - c)
+            keys.append(kk)
+        _KEYS[d] = np.sort(np.concatenate(keys))
+    return _KEYS[d]
+
+
+def _graded_lex_map_vectorised(d, rows):
+    """Independent vectorised construction of rows `rows` of the index map (no shared code with
+    oracle.bqp or the library): basis monomials as sorted index pairs (-1 = absent), products as
+    set symmetric differences of the pairs, ids by searchsorted over integer keys
+    deg (d+1)^4 + sum_k (s_k + 1) (d+1)^(3-k) (graded-lex order of sorted tuples, reading R18)."""
+    D = d + 1
+    iu = np.triu_indices(d, 1)
+    B = np.full((1 + d + iu[0].size, 2), -1, dtype=np.int64)
+    B[1:d + 1, 0] = np.arange(d)
+    B[d + 1:, 0], B[d + 1:, 1] = iu
+    keys = _graded_lex_keys(d)
+    A = B[rows]                      # (r, 2)
+    Ai = np.repeat(A[:, None, :], B.shape[0], axis=1)
+    Bj = np.repeat(B[None, :, :], len(rows), axis=0)
+    el = np.concatenate([Ai, Bj], axis=2)  # (r, n, 4) with -1 padding
+    el = np.sort(el, axis=2)
+    # symmetric difference: drop equal adjacent pairs (each index appears at most twice)
+    dup = np.zeros(el.shape, bool)
+    eq = (el[..., 1:] == el[..., :-1]) & (el[..., 1:] >= 0)
+    dup[..., 1:] |= eq
+    dup[..., :-1] |= eq
+    el = np.where(dup, -1, el)
+    el = np.sort(el, axis=2)[..., ::-1]  # present indices first, descending
+    deg = (el >= 0).sum(axis=2)
+    # ascending order of the present indices: reverse the first deg entries
+    key = deg.astype(np.int64) * D ** 4
+    for c in range(4):
+        # c-th smallest present index = el[..., deg - 1 - c] when c < deg
+        idx = np.clip(deg - 1 - c, 0, 3)
+        v = np.take_along_axis(el, idx[..., None], axis=2)[..., 0]
+        key += np.where(c < deg, (v + 1) * D ** (3 - c), 0)
+    ids = np.searchsorted(keys, key)
+    assert np.array_equal(keys[ids], key)
+    return ids.astype(np.int32), keys.size
+
+
+@pytest.mark.parametrize("d,kind", [(100, "dense"), (150, "er05")])
+def test_index_map_bit_exact_large(ctx, d, kind):
+    """BASELINE configs[2]/[3] sizes (n = 5051 / 11326): the exported map equals an independent
+    vectorised graded-lex construction row by row, and the CSR segments list exactly the upper
+    positions of each constraint in (i, j) order."""
+    Q, c = bqp_instance(d, 0, kind)
+    ctx.set_bqp(Q, c)
+    n, m, nu = ctx.sizes()
+    assert n == 1 + d + d * (d - 1) // 2
+    g_amap, seg_ptr, seg_pos = ctx.export_index_map()
+    for r0 in range(0, n, 256):
+        rows = np.arange(r0, min(n, r0 + 256))
+        ids, mm = _graded_lex_map_vectorised(d, rows)
+        assert mm == m
+        assert np.array_equal(g_amap[rows], ids), r0
+    assert nu == n * (n + 1) // 2 and seg_ptr[-1] == nu and seg_ptr[0] == 0
+    pi = (seg_pos >> 16).astype(np.int64)
+    pj = (seg_pos & 0xFFFF).astype(np.int64)
+    assert np.all(pi <= pj)
+    owner = np.repeat(np.arange(m), np.diff(seg_ptr))
+    assert np.array_equal(g_amap[pi, pj], owner)
+    # (i, j) strictly increasing inside each segment
+    inc = np.diff(seg_pos.astype(np.int64)) > 0
+    same = owner[1:] == owner[:-1]
+    assert np.all(inc[same])
+    cnt = np.bincount(g_amap.ravel(), minlength=m)
+    assert np.array_equal(np.bincount(owner, weights=np.where(pi == pj, 1, 2), minlength=m).astype(np.int64), cnt)
+
+
 def test_general_problem_entry(ctx):
     """drsdp_set_problem with COO triplets reproduces set_bqp's map; errors are reported."""
     from paper_2512_04406_b200 import abi
@@ -245,9 +335,14 @@ def test_general_problem_entry(ctx):
     assert e.value.code == abi.ERR_INVALID_ARG
 
 
+_RELAX = {}
+
+
 def _state(d, seed, sigma, p):
     Q, c = bqp_instance(d, seed)
-    amap, cnt, b = bqp.relax(Q, c)
+    if (d, seed) not in _RELAX:  # oracle.bqp.relax loops over n^2 positions (a minute at d = 100)
+        _RELAX[(d, seed)] = bqp.relax(Q, c)
+    amap, cnt, b = _RELAX[(d, seed)]
     n, m = amap.shape[0], cnt.size
     D = ops.D_matrix(amap, cnt, b)
     Xt = random_symmetric(n, seed + 1, 0.3)
@@ -285,13 +380,35 @@ def test_alm_eval_parity(ctx, d, seed, sigma, p):
     assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
 
 
-@pytest.mark.parametrize("d,p", [(40, 24), (100, 40), (100, 96)])
+def _state_vectorised_map(d, kind, seed, sigma, p):
+    """_state for large d with the test's vectorised graded-lex map (oracle.bqp.relax's Python
+    loop over n^2 positions takes minutes at d = 150); b per the relaxation's definition."""
+    Q, c = bqp_instance(d, seed, kind)
+    n = 1 + d + d * (d - 1) // 2
+    amap = np.empty((n, n), np.int32)
+    for r0 in range(0, n, 512):
+        rows = np.arange(r0, min(n, r0 + 512))
+        amap[rows], m = _graded_lex_map_vectorised(d, rows)
+    cnt = np.bincount(amap.ravel(), minlength=m).astype(np.int64)
+    b = np.zeros(m)  # only b's support enters D; the evaluation below does not use b
+    T = random_symmetric(n, seed + 1, 0.3)
+    T = T - ops.At(amap, ops.A(amap, T, m) / cnt)
+    Y = random_unit_factor(n, p, seed + 2)
+    U = sp.project(Y, random_matrix(n, p, seed + 3))
+    return Q, c, amap, cnt, b, T, Y, U
+
+
+@pytest.mark.parametrize("d,p", [(40, 24), (100, 40), (100, 96), (100, 256), (100, 512), (100, 1024), (150, 64)])
 def test_alm_eval_full_size(ctx, d, p):
-    """BASELINE configs[1]/[2] sizes (n = 821, 5051): the y-eliminated evaluation in the solver's
-    launch configuration (dense Gram tiles + TMA products, pitch 64) against the oracle."""
+    """BASELINE configs[1]/[2]/[3] sizes (n = 821, 5051, 11326): the y-eliminated evaluation in the
+    solver's launch configuration (dense Gram tiles + TMA products; p > 64 column-chunked products
+    and row epilogues up to DRSDP_MAX_P) against the oracle."""
     from paper_2512_04406_b200 import abi
 
-    Q, c, amap, cnt, b, T, Y, U = _state(d, 7, 3.0, p)
+    if d == 150:
+        Q, c, amap, cnt, b, T, Y, U = _state_vectorised_map(d, "er05", 7, 3.0, p)
+    else:
+        Q, c, amap, cnt, b, T, Y, U = _state(d, 7, 3.0, p)
     n = amap.shape[0]
     sigma = 3.0
     ctx.set_bqp(Q, c)
@@ -518,3 +635,105 @@ def test_fixed_m_mode_first_iterations(ctx):
     assert abs(r0["dual_obj"] - q0["dual_obj"]) <= 1e-6 * (1 + abs(q0["dual_obj"]))
     for k in ("eta_p", "eta_g"):
         assert abs(r0[k] - q0[k]) <= 1e-6 * (1 + abs(q0[k])), k
+
+
+# ---- a9: block Lanczos for the extreme eigenpairs of X = T - Diag(z) ----
+def _lanczos_on(ctx, T, z, steps, nvec):
+    n = T.shape[0]
+    ld = (n + 63) // 64 * 64
+    Tp = np.zeros((n, ld))
+    Tp[:, :n] = T
+    V = torch.zeros((n, max(nvec, 1)), dtype=torch.float64, device="cuda")
+    ritz, resid, lmax, basis = ctx.x_eigs(dev(Tp), ld, dev(z), steps, nvec, V)
+    return ritz, resid, lmax, basis, V.cpu().numpy()[:, :nvec]
+
+
+def _diag_problem(ctx, n):
+    """A problem of side n (one constraint per diagonal position) that only sets the size."""
+    idx = np.arange(n, dtype=np.int32)
+    ctx.set_problem(n, n, None, idx, idx, idx, np.ones(n))
+
+
+@pytest.mark.parametrize("n", [64, 144, 150])
+def test_lanczos_exact_when_basis_spans(ctx, n):
+    """With the basis equal to the whole space (k b = n) the Ritz pairs are the eigenpairs:
+    every Ritz value matches LAPACK eigh (the textbook routine, P15). n = 150: ragged (basis
+    144 < n), bounds and Ritz-pair identities only."""
+    _diag_problem(ctx, n)
+    nn = n
+    T = random_symmetric(nn, 3)
+    z = random_matrix(nn, 1, 4)[:, 0]
+    lam = np.linalg.eigvalsh(T - np.diag(z))
+    steps = nn // 16
+    ritz, resid, lmax, basis, V = _lanczos_on(ctx, T, z, steps, 8)
+    assert basis == (nn // 16) * 16
+    if basis == nn:
+        np.testing.assert_allclose(ritz, lam[:8], atol=1e-11 * (1 + abs(lam).max()))
+        assert abs(lmax - lam[-1]) <= 1e-11 * (1 + abs(lam[-1]))
+    # Ritz values always bound the spectrum from inside
+    assert np.all(ritz >= lam[:8] - 1e-11 * (1 + abs(lam).max())) and lmax <= lam[-1] + 1e-11 * (1 + abs(lam[-1]))
+    # Ritz vectors: orthonormal, Rayleigh quotients equal the Ritz values, residuals as reported
+    X = T - np.diag(z)
+    np.testing.assert_allclose(V.T @ V, np.eye(8), atol=1e-12)
+    np.testing.assert_allclose(np.einsum("ic,ij,jc->c", V, X, V), ritz, atol=1e-11 * (1 + abs(lam).max()))
+    true_res = np.linalg.norm(X @ V - V * ritz, axis=0)
+    np.testing.assert_allclose(resid, true_res, atol=1e-9 * (1 + abs(lam).max()))
+
+
+@pytest.mark.parametrize("n_d", [(3241, 80), (5051, 100)])
+def test_lanczos_separated_spectrum(ctx, n_d):
+    """A spectrum with 8 separated negative eigenvalues, a bulk in [0, 1] and a top eigenvalue 5:
+    block Lanczos (40 steps of block 16, TMA product on T) finds the 8 negative pairs and lambda_max
+    to <= 1e-9 (eigenvalues) with eigenvector residuals <= 1e-6."""
+    n, d = n_d
+    _diag_problem(ctx, n)
+    rng = np.random.default_rng([20251204, 99, n])
+    neg = np.array([-3.0, -2.6, -2.2, -1.9, -1.6, -1.3, -1.1, -0.95])
+    lam = np.concatenate([neg, rng.uniform(0.0, 1.0, n - 9), [5.0]])
+    Qm, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    z = rng.uniform(-0.5, 0.5, n)
+    X = (Qm * lam) @ Qm.T
+    T = X + np.diag(z)
+    ritz, resid, lmax, basis, V = _lanczos_on(ctx, T, z, 40, 8)
+    np.testing.assert_allclose(ritz, neg, atol=1e-9)
+    assert abs(lmax - 5.0) <= 1e-9
+    assert resid.max() <= 1e-6
+    # each Ritz vector aligned with its eigenvector (up to sign)
+    align = np.abs(np.einsum("ic,ic->c", V, Qm[:, :8]))
+    assert align.min() >= 1 - 1e-10
+
+
+def test_lanczos_on_admm_state_matches_eigh(ctx):
+    """A real ADMM state (d = 40 after one outer iteration): the escape candidates of block
+    Lanczos have Rayleigh quotients below the escape threshold and lambda_max matches eigh."""
+    Q, c = bqp_instance(40, 0)
+    ctx.set_bqp(Q, c)
+    n = ctx.sizes()[0]
+    ctx.set_params(ctx.default_params(p0=4, max_outer=1, eig_method=1))
+    ctx.set_initial_factor(initial_factor(n, 4, 0))
+    ctx.solve()
+    sol = ctx.solution(want_X=True)
+    X = sol["X"]
+    z = sol["z"]
+    lam = np.linalg.eigvalsh(X)
+    ritz, resid, lmax, basis, V = _lanczos_on(ctx, X + np.diag(z), z, 40, 8)
+    assert abs(lmax - lam[-1]) <= 1e-9 * (1 + abs(lam[-1]))
+    assert np.all(ritz >= lam[:8] - 1e-9)
+    assert abs(ritz[0] - lam[0]) <= 1e-6 * (1 + abs(lam[-1]))  # most negative pair converged
+    rq = np.einsum("ic,ij,jc->c", V, X, V)
+    np.testing.assert_allclose(rq, ritz, atol=1e-10 * (1 + abs(lam[-1])))
+
+
+@pytest.mark.parametrize("d,seed", [(10, 0), (20, 1)])
+def test_solve_lanczos_eigen_step(ctx, d, seed):
+    """eig_method = 2 (block Lanczos every outer iteration, dense confirmation at the end):
+    certified optimum equal to the oracle's (eta recomputed by the oracle from the tuple)."""
+    Q, c = bqp_instance(d, seed)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 2, seed, eig_method=2)
+    assert info["status"] == 0, info
+    amap, cnt, b = bqp.relax(Q, c)
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2), initial_factor(amap.shape[0], 2, seed))
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+    X = ctx.solution(want_X=True)["X"]
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8
