@@ -54,7 +54,8 @@ class Params:
         self.rho_reg = 1e3
         self.stall_rtr = 10
         self.max_tcg = 100
-        self.precond_mu = 0.0  # reading R35: Gram right-preconditioner of the truncated CG (0 = off)
+        self.precond_mu = -1.0  # reading R35: Gram right-preconditioner of the truncated CG (0 = off,
+                                # < 0 = auto: mu = 0.1 for n >= 2048, off below)
         self.escape_gate = 0.0  # reading R36: escape / rank change only after an inner solve within
                                 # escape_gate x its tolerance (0 = always)
         for k, v in kw.items():
@@ -162,7 +163,8 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         grad_tol = 4.0 * eps_k / sigma  # f scale: ||XY|| = sigma/4 ||R||
         Y, info = rtr(prob, Y, RTRParams(n, p, max_iter=prm.max_rtr, rho_reg=prm.rho_reg,
                                         max_tcg=prm.max_tcg if prm.max_tcg > 0 else None,
-                                        precond_mu=prm.precond_mu), grad_tol, warm_U=U,
+                                        precond_mu=(prm.precond_mu if prm.precond_mu >= 0 else
+                                                    (0.1 if n >= 2048 else 0.0))), grad_tol, warm_U=U,
                       stall=prm.stall_rtr)
         totals["rtr"] += info["iters"]
         totals["tcg"] += info["tcg"]

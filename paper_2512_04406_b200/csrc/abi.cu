@@ -134,18 +134,18 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     return prof_kind ? prof_end(ctx) : DRSDP_OK;
   }
   if (!no_tma && symv_tma_supported(a, epi, mode2, atr)) {
-    const int pt = symv_pt(a.p), bm = symv_tma_rows(), bk = symv_tma_kstep();
+    const int pt = symv_tma_pt(a.p, epi), bm = symv_tma_rows(), bk = symv_tma_kstep();
     const bool pair = mode2 == MODE2_PAIR;
     const int kn = a.ncols > 0 ? a.ncols : a.n;
     const int ktot = pair ? 2 * ((kn + bk - 1) / bk * bk) : kn;
-    const int ntiles = ((a.n + bm - 1) / bm) * symv_chunks(a.p, epi);
+    const int ntiles = ((a.n + bm - 1) / bm) * symv_tma_chunks(a.p, epi);
     // split-K: one CTA per SM (the ring uses most of shared memory); waves x k-rows cost model
     int S = 1;
     double best = 1e300;
     for (int s = 1; s <= 64; ++s) {
       const int per = ((ktot + s - 1) / s + bk - 1) / bk * bk;
       if (s > 1 && (int64_t)(s - 1) * per >= ktot) break;
-      const int slots = ctx->num_sms * symv_tma_ctas_per_sm(a.p);
+      const int slots = ctx->num_sms * symv_tma_ctas_per_sm(pt);
       const int waves = (ntiles * s + slots - 1) / slots;
       const double cost = (double)waves * (per + 64) + 24.0 * s;
       if (cost < best * 0.999) {
@@ -1057,7 +1057,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->seed = 0;
   o->rho_reg = 1e3;
   o->stall_rtr = 10;
-  o->precond_mu = 0.0;
+  o->precond_mu = -1.0;  // auto (reading R35)
   o->escape_gate = 0.0;
   return DRSDP_OK;
 }
@@ -1068,7 +1068,7 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
-        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.precond_mu >= 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
+        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
         q.escape_gate >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;

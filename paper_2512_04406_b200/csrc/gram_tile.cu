@@ -29,19 +29,34 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * 8 + 1024;
 
 }  // namespace
 
+// upper tile t (row-major over I <= J) -> (I, J)
+DRSDP_DEV void upper_tile(int t, int nb, int &I, int &J) {
+  I = 0;
+  while (t >= nb - I) {
+    t -= nb - I;
+    ++I;
+  }
+  J = I + t;
+}
+
+// One CTA per upper tile (I <= J; D is symmetric and its consumers read i <= j). The contraction
+// runs over 16-column TMA boxes of the concatenated K = [A1 | A2] (p columns each, the last box of
+// each operand zero-filled past p): a stage holds two consecutive boxes, so at p <= 16 the pair
+// product [Y U][U Y]^T is a single stage of 32 useful columns.
 __global__ void __launch_bounds__(NT, 1)
     gram_tile_kernel(const __grid_constant__ CUtensorMap mA1, const __grid_constant__ CUtensorMap mB1,
                      const __grid_constant__ CUtensorMap mA2, const __grid_constant__ CUtensorMap mB2, int n, int p,
                      int pair, double *__restrict__ D, int64_t ldd, const int *skip) {
-  const int I = blockIdx.y, J = blockIdx.x;
-  if (I > J) return;  // upper-triangle tiles only (D symmetric; consumers read i <= j)
+  int I, J;
+  upper_tile(blockIdx.x, (n + TB - 1) / TB, I, J);
   if (skip && *(volatile const int *)skip) return;
   extern __shared__ unsigned char smem_raw[];
   double *smem = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nk1 = (p + BK - 1) / BK;
-  const int nk = pair ? 2 * nk1 : nk1;
+  const int nbx1 = (p + 15) / 16;              // 16-column boxes per operand
+  const int nbx = pair ? 2 * nbx1 : nbx1;
+  const int nk = (nbx + 1) / 2;                 // stages of two boxes
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       bar_init(&full[s], 1);
@@ -56,14 +71,17 @@ __global__ void __launch_bounds__(NT, 1)
         const int st = kt % STAGES;
         if (kt >= STAGES) bar_wait(&empty[st], ((kt / STAGES) - 1) & 1);
         double *sa = smem + st * STAGE_ELEMS, *sb = sa + OP_ELEMS;
-        const bool second = kt >= nk1;
-        const int k0 = (second ? kt - nk1 : kt) * BK;
-        const CUtensorMap *ma = second ? &mA2 : &mA1, *mb = second ? &mB2 : &mB1;
         bar_expect(&full[st], STAGE_BYTES);
-        tma2d(sa, ma, k0, I * TB, &full[st]);
-        tma2d(sa + TB * 16, ma, k0 + 16, I * TB, &full[st]);
-        tma2d(sb, mb, k0, J * TB, &full[st]);
-        tma2d(sb + TB * 16, mb, k0 + 16, J * TB, &full[st]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int bx = 2 * kt + h;  // box index in the concatenated K (past the end: zero-filled)
+          const bool second = bx >= nbx1 && bx < nbx;
+          // bx >= nbx: a box entirely past column p of A1 (TMA zero-fills out-of-range elements)
+          const int c0 = bx >= nbx ? nbx1 * 16 : (second ? bx - nbx1 : bx) * 16;
+          const CUtensorMap *ma = second ? &mA2 : &mA1, *mb = second ? &mB2 : &mB1;
+          tma2d(sa + h * TB * 16, ma, c0, I * TB, &full[st]);
+          tma2d(sb + h * TB * 16, mb, c0, J * TB, &full[st]);
+        }
       }
     }
     return;
@@ -138,7 +156,8 @@ cudaError_t gram_tile_launch(int n, int p, const double *A1, const double *B1, c
     attr = true;
   }
   const int nb = (n + TB - 1) / TB;
-  gram_tile_kernel<<<dim3(nb, nb), NT, SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], n, p, pair ? 1 : 0, D, ldd, skip);
+  gram_tile_kernel<<<nb * (nb + 1) / 2, NT, SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], n, p, pair ? 1 : 0, D, ldd,
+                                                              skip);
   return cudaGetLastError();
 }
 

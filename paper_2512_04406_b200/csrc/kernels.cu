@@ -893,16 +893,20 @@ __global__ void __launch_bounds__(256) gather_assemble_kernel(int n, const int32
                                                               const double *__restrict__ w, double *__restrict__ W,
                                                               int64_t ldw, const int *skip) {
   if (skip && *(volatile const int *)skip) return;
-  const int64_t total = (int64_t)n * ldw;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ldw, j = e - i * ldw;
-    double v = 0.0;
-    if (j < n) {
-      const int32_t id = __ldg(amap + i * ldmap + j);
-      if (id >= 0) v = __ldg(w + id);
-    }
-    W[e] = v;
-  }
+  // row = blockIdx.y, four consecutive columns per thread (ldw, ldmap are multiples of 4): one
+  // int4 load of ids, four gathers of w (L2-resident), two double2 stores
+  const int64_t i = blockIdx.y;
+  const int j = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (j >= ldw) return;
+  int4 id = make_int4(-1, -1, -1, -1);
+  if (j < n) id = __ldg(reinterpret_cast<const int4 *>(amap + i * ldmap + j));
+  const int ids[4] = {id.x, id.y, id.z, id.w};
+  double v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = (j + k < n && ids[k] >= 0) ? __ldg(w + ids[k]) : 0.0;
+  double2 *out = reinterpret_cast<double2 *>(W + i * ldw + j);
+  out[0] = make_double2(v[0], v[1]);
+  out[1] = make_double2(v[2], v[3]);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1025,7 +1029,9 @@ cudaError_t tcg_finalize_launch(int n, int p, int ld, const TcgDev *st, double *
 
 cudaError_t gather_assemble_launch(int n, const int32_t *amap, int64_t ldmap, const double *w, double *W, int64_t ldw,
                                    const int *skip, cudaStream_t st) {
-  gather_assemble_kernel<<<1184, 256, 0, st>>>(n, amap, ldmap, w, W, ldw, skip);
+  if ((ldw & 3) || (ldmap & 3) || n > 65535) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((ldw / 4 + 255) / 256), (unsigned)n);
+  gather_assemble_kernel<<<grid, 256, 0, st>>>(n, amap, ldmap, w, W, ldw, skip);
   return cudaGetLastError();
 }
 

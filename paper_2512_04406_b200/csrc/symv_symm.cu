@@ -36,7 +36,11 @@ template <int PT>
 struct SCfg {
   static constexpr int CB = PT / 8;              // column fragments
   static constexpr int WM = BM / NCW, JB = WM / 8;  // forward warp tile 16 x PT
-  static constexpr int STAGES = PT >= 16 ? 2 : 3;  // PT = 16: 2 CTAs per SM (88 KB each)
+  // PT = 16: V_I^T fragments held in registers for the transposed product (VREG), one CTA per SM
+  // with a 4-stage ring; PT = 8: two CTAs per SM, 3 stages
+  static constexpr bool VREG = PT >= 16;
+  static constexpr int CTAS = PT >= 16 ? 1 : 2;
+  static constexpr int STAGES = PT >= 16 ? 4 : 3;
   static constexpr int A_ELEMS = BM * BK, V_ELEMS = PT * BK;
   static constexpr int STAGE_ELEMS = A_ELEMS + V_ELEMS;
   static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
@@ -49,7 +53,7 @@ struct SCfg {
 }  // namespace
 
 template <int PT>
-__global__ void __launch_bounds__(NTA, 2)
+__global__ void __launch_bounds__(NTA, SCfg<PT>::CTAS)
     symm_partial_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
                         const int4 *__restrict__ units, double *__restrict__ Fpart, double *__restrict__ Tpart,
                         const int *skip) {
@@ -100,9 +104,26 @@ __global__ void __launch_bounds__(NTA, 2)
 #pragma unroll
     for (int cb = 0; cb < C::CB; ++cb) acc[jb][cb][0] = acc[jb][cb][1] = 0.0;
   bar_wait(&vi_bar, 0);
-  // transposed fragment of this warp (warps < NTF): rows kf*8.. of the stage, columns cf*8..
-  const int kf = warp / C::CB, cf = warp % C::CB;
-  const bool tw = warp < C::NTF;
+  // transposed part: warp -> (cf, kb): output columns cf*8.. (of V) and the 8 columns kb*8.. of each
+  // 32-wide stage (rows k of block J). The contraction runs over the 128 rows i of block I; the
+  // A operand V_I^T is fixed for the whole unit and lives in registers (vf), the B operand is the
+  // stage's M fragment. The 4 rows i of k-step s are 8 (s/2) + 2 (s%2) + {0, 4, 1, 5}[r], so the
+  // rows of a fragment differ pairwise in bit 2 and the swizzled M loads take the minimal 2
+  // wavefronts; 4 independent accumulator chains (summed in fixed order) hide the DMMA latency.
+  // (PT = 16, C::VREG; PT = 8 keeps the shared-memory V_I operand of warps kf = warp / CB < 4)
+  const int cf = warp % C::CB, kb = warp / C::CB;
+  const bool tw = kb < BK / 8;
+  const int roff = (r >> 1) + 4 * (r & 1);
+  const int kf = warp / C::CB;
+  const bool twold = warp < C::NTF;
+  double vf[C::VREG ? BM / 4 : 1];
+  if constexpr (C::VREG) {
+#pragma unroll
+    for (int ks = 0; ks < BM / 4; ++ks) {
+      const int i = 8 * (ks >> 1) + 2 * (ks & 1) + roff;
+      vf[ks] = tw ? ldsw(vi + (i >> 4) * PT * 128, cf * 8 + q, i & 15) : 0.0;
+    }
+  }
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt % C::STAGES;
     bar_wait(&full[st], (kt / C::STAGES) & 1);
@@ -123,30 +144,53 @@ __global__ void __launch_bounds__(NTA, 2)
         for (int cb = 0; cb < C::CB; ++cb) dmma_884(acc[jb][cb][0], acc[jb][cb][1], af[jb], bf[cb]);
     }
     const int J = Ja + kt / (BM / BK), s = kt % (BM / BK);
-    if (J > I && tw) {
-      // out[k][c] = sum_i M[i][k] V_I[i][c] for k = kf*8 + q of this stage. The contraction rows
-      // of k-step ks are i = 8 (ks/2) + 2 (ks%2) + {0, 4, 1, 5}[r], so that the 4 rows of a
-      // fragment differ in bit 2 pairwise and the swizzled loads of M (column access) and of
-      // V_I^T take the minimal 2 wavefronts; 4 independent accumulator chains (summed in a fixed
-      // order) hide the DMMA latency.
-      double t[4][2];
+    if constexpr (C::VREG) {
+      if (J > I && tw) {
+        // out^T[c][k] = sum_i V_I^T[c][i] M[i][k]: D (8 c x 8 k) += A (V_I^T, registers) B (M, shared)
+        double t[4][2];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) t[c][0] = t[c][1] = 0.0;
-      const int kk = kf * 8 + q;  // column within the 32-wide stage
-      const uint32_t ba = sa + (kk >> 4) * BM * 128;
-      const int roff = (r >> 1) + 4 * (r & 1);
-#pragma unroll 8
-      for (int ks = 0; ks < BM / 4; ++ks) {
-        const int i = 8 * (ks >> 1) + 2 * (ks & 1) + roff;
-        const double av = ldsw(ba, i, kk & 15);
-        const double bv2 = ldsw(vi + (i >> 4) * PT * 128, cf * 8 + q, i & 15);
-        dmma_884(t[ks & 3][0], t[ks & 3][1], av, bv2);
+        for (int c = 0; c < 4; ++c) t[c][0] = t[c][1] = 0.0;
+        const int kk = kb * 8 + q;  // B fragment column = k within the stage
+        const uint32_t ba = sa + (kk >> 4) * BM * 128;
+#pragma unroll
+        for (int ks = 0; ks < BM / 4; ++ks) {
+          const int i = 8 * (ks >> 1) + 2 * (ks & 1) + roff;
+          const double bm = ldsw(ba, i, kk & 15);
+          dmma_884(t[ks & 3][0], t[ks & 3][1], vf[ks], bm);
+        }
+        const double t0 = (t[0][0] + t[1][0]) + (t[2][0] + t[3][0]);
+        const double t1 = (t[0][1] + t[1][1]) + (t[2][1] + t[3][1]);
+        // D[c = cf*8 + q][k = kb*8 + 2r + {0, 1}] -> partial tile T[J][I] (rows k, columns c)
+        double *tp = Tpart + ((size_t)J * (J - 1) / 2 + I) * C::TILE;
+        const int row = s * BK + kb * 8 + 2 * r, colo = cf * 8 + q;
+        tp[row * PT + colo] = t0;
+        tp[(row + 1) * PT + colo] = t1;
       }
-      const double t0 = (t[0][0] + t[1][0]) + (t[2][0] + t[3][0]);
-      const double t1 = (t[0][1] + t[1][1]) + (t[2][1] + t[3][1]);
-      double *tp = Tpart + ((size_t)J * (J - 1) / 2 + I) * C::TILE;
-      const int row = s * BK + kf * 8 + q, colo = cf * 8 + 2 * r;
-      *reinterpret_cast<double2 *>(tp + row * PT + colo) = make_double2(t0, t1);
+    } else {
+      if (J > I && twold) {
+        // out[k][c] = sum_i M[i][k] V_I[i][c] for k = kf*8 + q of this stage. The contraction rows
+        // of k-step ks are i = 8 (ks/2) + 2 (ks%2) + {0, 4, 1, 5}[r], so that the 4 rows of a
+        // fragment differ in bit 2 pairwise and the swizzled loads of M (column access) and of
+        // V_I^T take the minimal 2 wavefronts; 4 independent accumulator chains (summed in a fixed
+        // order) hide the DMMA latency.
+        double t[4][2];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) t[c][0] = t[c][1] = 0.0;
+        const int kk = kf * 8 + q;  // column within the 32-wide stage
+        const uint32_t ba = sa + (kk >> 4) * BM * 128;
+#pragma unroll 8
+        for (int ks = 0; ks < BM / 4; ++ks) {
+          const int i = 8 * (ks >> 1) + 2 * (ks & 1) + roff;
+          const double av = ldsw(ba, i, kk & 15);
+          const double bv2 = ldsw(vi + (i >> 4) * PT * 128, cf * 8 + q, i & 15);
+          dmma_884(t[ks & 3][0], t[ks & 3][1], av, bv2);
+        }
+        const double t0 = (t[0][0] + t[1][0]) + (t[2][0] + t[3][0]);
+        const double t1 = (t[0][1] + t[1][1]) + (t[2][1] + t[3][1]);
+        double *tp = Tpart + ((size_t)J * (J - 1) / 2 + I) * C::TILE;
+        const int row = s * BK + kf * 8 + q, colo = cf * 8 + 2 * r;
+        *reinterpret_cast<double2 *>(tp + row * PT + colo) = make_double2(t0, t1);
+      }
     }
     __syncwarp();
     if (lane == 0) bar_arrive(&empty[st]);

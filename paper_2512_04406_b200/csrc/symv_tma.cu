@@ -230,6 +230,14 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
 }
 
 int symv_tma_rows() { return BM; }
+// column chunk width of the TMA kernel (raw products with p > 64 run in 64-wide chunks: a 128-wide
+// variant, measured on B200 at n = 5051, p = 128 / 512, was no faster — the re-reads of M by the
+// chunks hit L2 — and needs 168 registers with spills at 288 threads)
+int symv_tma_pt(int p, int epi) {
+  (void)epi;
+  return symv_pt(p);
+}
+int symv_tma_chunks(int p, int epi) { return epi == EPI_RAW ? (p + symv_tma_pt(p, epi) - 1) / symv_tma_pt(p, epi) : 1; }
 int symv_tma_ctas_per_sm(int p) { return symv_pt(p) <= 16 ? 2 : 1; }
 int symv_tma_kstep() { return BK; }
 
@@ -243,7 +251,7 @@ static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap *m, int S, 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int nz = EPI == EPI_RAW ? (a.p + PT - 1) / PT : 1;
+  const int nz = EPI == EPI_RAW ? (a.p + PT - 1) / PT : 1;  // = symv_tma_chunks
   dim3 grid((a.n + BM - 1) / BM, S, nz);
   k<<<grid, NTHREADS, C::SMEM_BYTES, st>>>(m[0], m[1], m[2], m[3], a);
   return cudaGetLastError();
@@ -268,7 +276,7 @@ static cudaError_t tma_dispatch(const SymvArgs &a, int epi, bool pair, const CUt
 // Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR), ldvt = round_up(kn, 2), kn =
 // the contraction length (ncols in row-block mode, else n)
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st) {
-  const int pt = symv_pt(a.p);
+  const int pt = symv_tma_pt(a.p, epi);
   const bool pair = a.A2 != nullptr;
   const int kn = a.ncols > 0 ? a.ncols : a.n;
   dim3 tg((kn + 31) / 32, (a.p + 31) / 32);
