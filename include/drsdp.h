@@ -125,7 +125,7 @@ typedef struct {
                                           stall_rtr iterations and is within 100x of the inner
                                           tolerance (0 = never; reading R30)                       */
   int32_t eig_method;                  /* eigen step (eta_d, escape directions): 0 = auto (block
-                                          Lanczos for n >= 2048, dense dsyevd below), 1 = dense dsyevd
+                                          Lanczos for n >= 16384, dense dsyevd below), 1 = dense dsyevd
                                           every outer iteration, 2 = block Lanczos always. With
                                           Lanczos, convergence (eta_max <= tol) is confirmed by one dense
                                           decomposition before the solve returns OK                    */

@@ -11,6 +11,9 @@ subproblem formulas): it only draws the random data that both sides receive
   fixes U[-1,1], which governs.)
 * ``sweep_inputs(n, p)`` — the subproblem-kernel sweep of config 4: M symmetric
   with entries N(0,1)/sqrt(n), Y with unit rows, U a random tangent direction.
+* ``chain_bqp_instance(q, t, seed)`` — the sparse (clique-chain) BQP of PAPER.md:555-579
+  (SURVEY §8(f) row f2): t cliques of q variables, Q_k symmetric with [Q_k]_ij ~ N(0,1)
+  (i <= j, mirrored), c_k ~ N(0,1)^q, as the paper draws them (no BASELINE config).
 * ``initial_factor(n, p, seed)`` — the random starting point Y^0 the method
   draws (PAPER.md:321 writes Y^0 = 0, not a manifold point; reading R1),
   passed as an input to both the oracle and the GPU solver.
@@ -38,6 +41,21 @@ def bqp_instance(d: int, seed: int = 0, kind: str = "dense"):
     Q = Q + Q.T
     c = rng.uniform(-1.0, 1.0, d)
     return Q, c
+
+
+def chain_bqp_instance(q: int, t: int, seed: int = 0):
+    """Return (Qs [t, q, q], cs [t, q]) for the clique-chain BQP."""
+    if q < 2 or t < 1:
+        raise ValueError("need q >= 2, t >= 1")
+    rng = np.random.default_rng([SEED, 23, q, t, seed])
+    iu = np.triu_indices(q)
+    Qs = np.zeros((t, q, q))
+    for k in range(t):
+        A = np.zeros((q, q))
+        A[iu] = rng.standard_normal(iu[0].size)
+        Qs[k] = A + np.triu(A, 1).T
+    cs = rng.standard_normal((t, q))
+    return Qs, cs
 
 
 def _unit_rows(A: np.ndarray) -> np.ndarray:
