@@ -497,6 +497,30 @@ def run_gpu(args):
                            "eta_p": info["eta_p"], "eta_d": info["eta_d"], "eta_g": info["eta_g"],
                            "dual_obj": info["dual_obj"], "n_costgrad": info["n_costgrad"], "n_hvp": info["n_hvp"]})
         out["solves"] = solves
+        # clique-chain sparse BQPs (multi-block relaxation), N(0,1) data as
+        # in the paper; the paper's ManiDSDP means (Tables 2-3) as context
+        from inputs import chain_bqp_instance
+
+        paper_chain = {(20, 20): 10.3, (20, 40): 48.4, (20, 60): 100.7, (20, 80): 189.0, (20, 100): 166.3,
+                       (20, 120): 312.0, (10, 10): 0.18, (20, 10): 4.21, (30, 10): 62.9, (40, 10): 812.0}
+        chain = []
+        for q, t in args.solve_chain:
+            Qs, cs = chain_bqp_instance(q, t, 0)
+            ctx.set_bqp_chain(Qs, cs)
+            nn = ctx.sizes()[0]
+            ctx.set_params(ctx.default_params(p0=2, time_limit_s=args.solve_time_limit, **args.solve_params))
+            ctx.set_initial_factor(initial_factor(nn, 2, 0))
+            t0 = time.perf_counter()
+            info = ctx.solve()
+            wall = time.perf_counter() - t0
+            chain.append({"q": q, "t": t, "seed": 0, "n_rows": nn, "n_b": ctx.block_sizes()[1], "m": ctx.sizes()[1],
+                          "seconds": wall, "paper_mean_seconds": paper_chain.get((q, t)),
+                          "paper_context": "ManiDSDP, MATLAB on an i9-10900 CPU, Tables 2-3 (P:582-672); context only",
+                          "status": "converged" if info["status"] == 0 else "not_converged",
+                          "outer_iters": info["outer_iters"], "p_max": info["p_max"], "eta_p": info["eta_p"],
+                          "eta_d": info["eta_d"], "eta_g": info["eta_g"], "dual_obj": info["dual_obj"],
+                          "n_costgrad": info["n_costgrad"], "n_hvp": info["n_hvp"]})
+        out["chain_solves"] = chain
 
     # ---------------- cpu baseline (oracle, bounded sample) ------------------------------------
     if rank == 0 and not args.no_cpu_baseline:
@@ -538,6 +562,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-oracle", action="store_true")
     ap.add_argument("--solve-d", type=lambda s: [int(x) for x in s.split(",") if x], default=[10, 40, 80])
+    ap.add_argument("--solve-chain", type=lambda s: [tuple(int(v) for v in x.split(":")) for x in s.split(",") if x],
+                    default=[(20, 20), (20, 120)], help="clique-chain solves q:t,... (multi-block relaxation)")
     ap.add_argument("--solve-time-limit", type=float, default=120.0)
     ap.add_argument("--solve-params", type=lambda s: {k: (float(v) if "." in v or "e" in v else int(v))
                                                       for k, v in (a.split("=") for a in s.split(",") if a)},

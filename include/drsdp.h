@@ -90,6 +90,42 @@ int drsdp_set_problem(drsdp_ctx *ctx, int64_t n, int64_t m, const double *C, int
  * Q d*d symmetric, c length d. Requires 1 <= d <= 360 (n < 65536). */
 int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c);
 
+/* ---------------------------------------------------------------------------------------------
+ * Multi-block problems (remark P:434-436: Algorithm 2 on multi-block SDPs;
+ * the sparse BQP relaxation DSDP-sparse). S = diag(S_1, .., S_t), every block
+ * S_k = Y_k Y_k^T in S^+_{nb}, diag S_k = 1; one y per constraint, SHARED by all blocks whose
+ * positions it owns; C = 0. The factor Y stacks the blocks' rows: n = t * nb rows (block k owns
+ * rows k*nb .. (k+1)*nb - 1); only the diagonal blocks exist. Uniform block size nb.
+ * Solver differences (readings R37-R39): no tCG preconditioner; the eigen step is one
+ * batched decomposition of all blocks (cusolverDnXsyevBatched), eta_d and the escape directions
+ * from the union of the blocks' spectra; p <= min(64, nb); ALM mode only.
+ * Every call below (solve, alm_eval, y_update, dual_update, get_solution, export_index_map)
+ * accepts a block problem with these layouts:
+ *   T, M (device): n x ldt "stacked" — row r holds the nb columns of its block (ldt >= nb);
+ *   export_index_map: amap n*nb (row r, local column j); seg_pos packs GLOBAL rows (r<<16)|r';
+ *   get_solution: X is t column-major nb x nb blocks (t*nb*nb doubles).
+ * drsdp_assemble_M and drsdp_x_eigs are dense-only (ERR_INVALID_ARG).
+ * ------------------------------------------------------------------------------------------- */
+
+/* General uniform multi-block problem. HOST inputs: amaps t*nb*nb int32 (block k row-major at
+ * amaps + k*nb*nb; ids in [0, m), each block symmetric; every constraint owns >= 1 position,
+ * Assumption 2), b length m. Requires t*nb < 65536. Errors: INVALID_ARG, NOT_SYMMETRIC,
+ * SINGULAR_AAT (empty constraint); on error the previous problem is kept. */
+int drsdp_set_blocks(drsdp_ctx *ctx, int32_t t, int32_t nb, int64_t m, const int32_t *amaps, const double *b);
+
+/* Clique-chain sparse BQP relaxation: cliques x_k = {x_{(q-2)k}, .., x_{(q-2)k+q-1}}
+ * (0-based, k < t; consecutive cliques share two variables), objective
+ * sum_k x_k^T Q_k x_k + c_k^T x_k over {-1,1}^d, d = (q-2)t + 2. One block per clique with basis
+ * v(x_k) = [1, x_k, products of two clique variables] (graded-lex, nb = 1 + q + q(q-1)/2); one
+ * constraint per square-free monomial of degree <= 4 of some clique, ids in graded-lex order of
+ * sorted global index tuples; b_1 = sum_k tr Q_k, b_{x_i} = sum_k c_{k,i}, b_{x_ix_j} =
+ * sum_k 2 Q_{k,ij}, degree 3-4 -> 0. HOST inputs: Q t*q*q (block k row-major, symmetric), c t*q.
+ * Requires q >= 2, t*nb < 65536. */
+int drsdp_set_bqp_chain(drsdp_ctx *ctx, int32_t q, int32_t t, const double *Q, const double *c);
+
+/* Block structure of the current problem: t and nb (t = 0 and nb = n for a dense problem). */
+int drsdp_get_block_sizes(drsdp_ctx *ctx, int32_t *t, int32_t *nb);
+
 /* Sizes of the current problem (n, m, and the number of upper-triangle positions owned by
  * some constraint). Any output pointer may be NULL. */
 int drsdp_get_sizes(drsdp_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_upper);

@@ -258,7 +258,7 @@ def block_escape_directions(lams, Vs, eig_neg_tol, escape_max):
 def solve_blocks(amaps, cnt, b, prm: Params, Y0: np.ndarray, verbose=False):
     """Algorithm 2 on the multi-block problem, C = 0.
     Same control flow and readings as oracle/admm.solve; the tCG preconditioner (R35) is off
-    for block problems unless precond_mu > 0 is given (reading R37).
+    for block problems (reading R37).
     Parity unpinned: the trajectory (see oracle/admm.py)."""
     t0 = time.perf_counter()
     t, nb = amaps.shape[0], amaps.shape[1]
@@ -284,7 +284,7 @@ def solve_blocks(amaps, cnt, b, prm: Params, Y0: np.ndarray, verbose=False):
         grad_tol = 4.0 * eps_k / sigma
         Y, info = rtr(prob, Y, RTRParams(N, p, max_iter=prm.max_rtr, rho_reg=prm.rho_reg,
                                         max_tcg=prm.max_tcg if prm.max_tcg > 0 else None,
-                                        precond_mu=max(0.0, prm.precond_mu)), grad_tol, warm_U=U,
+                                        precond_mu=0.0), grad_tol, warm_U=U,
                       stall=prm.stall_rtr)
         totals["rtr"] += info["iters"]
         totals["tcg"] += info["tcg"]

@@ -20,7 +20,7 @@ TRACE_COLUMNS = ("iter", "eta_p", "eta_d", "eta_g", "eta_max", "primal_obj", "du
                  "inner_iters", "cg_iters", "escape_delta", "time_s")
 
 EXPORTED = ("drsdp_create", "drsdp_destroy", "drsdp_last_error", "drsdp_sync", "drsdp_set_problem",
-            "drsdp_set_bqp", "drsdp_get_sizes", "drsdp_export_index_map", "drsdp_default_params",
+            "drsdp_set_bqp", "drsdp_set_blocks", "drsdp_set_bqp_chain", "drsdp_get_block_sizes", "drsdp_get_sizes", "drsdp_export_index_map", "drsdp_default_params",
             "drsdp_set_params", "drsdp_set_initial_factor", "drsdp_solve", "drsdp_get_solution",
             "drsdp_get_trace", "drsdp_set_subproblem_matrix", "drsdp_set_subproblem_rows", "drsdp_subproblem_eval",
             "drsdp_subproblem_eval_host", "drsdp_assemble_M", "drsdp_y_update", "drsdp_dual_update",
@@ -77,6 +77,9 @@ def load_library():
         "drsdp_sync": (C.c_int, [vp]),
         "drsdp_set_problem": (C.c_int, [vp, i64, i64, dp, i64, dp, dp, dp, dp]),
         "drsdp_set_bqp": (C.c_int, [vp, i32, dp, dp]),
+        "drsdp_set_blocks": (C.c_int, [vp, i32, i32, i64, dp, dp]),
+        "drsdp_set_bqp_chain": (C.c_int, [vp, i32, i32, dp, dp]),
+        "drsdp_get_block_sizes": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32)]),
         "drsdp_get_sizes": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
         "drsdp_export_index_map": (C.c_int, [vp, dp, dp, dp]),
         "drsdp_default_params": (C.c_int, [C.POINTER(Params)]),
@@ -173,6 +176,24 @@ class Context:
         c = _host(c, np.float64)
         return self._check(self.lib.drsdp_set_bqp(self.h, Q.shape[0], _ptr(Q), _ptr(c)))
 
+    def set_blocks(self, amaps, b):
+        """Uniform multi-block problem: amaps (t, nb, nb) int32, b (m,) (drsdp_set_blocks)."""
+        amaps = _host(amaps, np.int32)
+        b = _host(b, np.float64)
+        t, nb = amaps.shape[0], amaps.shape[1]
+        return self._check(self.lib.drsdp_set_blocks(self.h, t, nb, b.size, _ptr(amaps), _ptr(b)))
+
+    def set_bqp_chain(self, Qs, cs):
+        """Clique-chain sparse BQP relaxation: Qs (t, q, q), cs (t, q) (drsdp_set_bqp_chain)."""
+        Qs = _host(Qs, np.float64)
+        cs = _host(cs, np.float64)
+        return self._check(self.lib.drsdp_set_bqp_chain(self.h, Qs.shape[1], Qs.shape[0], _ptr(Qs), _ptr(cs)))
+
+    def block_sizes(self):
+        t, nb = C.c_int32(), C.c_int32()
+        self._check(self.lib.drsdp_get_block_sizes(self.h, C.byref(t), C.byref(nb)))
+        return t.value, nb.value
+
     def sizes(self):
         n, m, nu = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(self.lib.drsdp_get_sizes(self.h, C.byref(n), C.byref(m), C.byref(nu)))
@@ -180,7 +201,8 @@ class Context:
 
     def export_index_map(self):
         n, m, nu = self.sizes()
-        amap = np.empty((n, n), np.int32)
+        t, nb = self.block_sizes()
+        amap = np.empty((n, nb), np.int32)  # dense: nb = n; blocks: stacked rows
         sp = np.empty(m + 1, np.int64)
         pos = np.empty(nu, np.uint32)
         self._check(self.lib.drsdp_export_index_map(self.h, _ptr(amap), _ptr(sp), _ptr(pos)))
@@ -217,7 +239,8 @@ class Context:
         p = C.c_int32()
         self._check(self.lib.drsdp_get_solution(self.h, None, None, C.byref(p), None, None))
         Y = np.empty((n, p.value))
-        X = np.empty((n, n)) if want_X else None
+        t, nb = self.block_sizes()
+        X = (np.empty((t, nb, nb)) if t else np.empty((n, n))) if want_X else None
         self._check(self.lib.drsdp_get_solution(self.h, _ptr(y), _ptr(Y), C.byref(p), _ptr(z), _ptr(X)))
         return {"y": y, "Y": Y, "z": z, "X": X, "p": p.value}
 

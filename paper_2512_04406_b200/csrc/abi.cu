@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "gram_tile.cuh"
 #include "symv.cuh"
+#include "blocks.cuh"
 
 using namespace drsdp;
 
@@ -371,6 +372,7 @@ static int hvp_generic(drsdp_ctx *ctx, int n, int p, const double *M, int64_t ld
 // z = rowdot(T Y, Y), sum z -> zsum (any p)
 int rowdot_product(drsdp_ctx *ctx, int n, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z,
                    double *zsum) {
+  if (ctx->prob.nblk > 0) return blk_rowdot(ctx, p, T, ldt, Y, ldv, z, zsum);
   if (p <= 64) {
     SymvArgs a = base_symv(ctx, n, p, T, ldt);
     a.V = Y;
@@ -511,6 +513,62 @@ static SegArgs seg_args(drsdp_ctx *ctx, int p, const double *Y, const double *U,
   return s;
 }
 
+// ----------------------------------------------------------------------------------------------
+// multi-block problems (blocks.cu): the same evaluations over the diagonal blocks
+// ----------------------------------------------------------------------------------------------
+static int blk_tiles(drsdp_ctx *ctx, SymvArgs &a) {
+  const Problem &P = ctx->prob;
+  CK(ctx->tile_scal.ensure((size_t)blk_product_tiles((int)P.nblk, (int)P.nb) * 2), "alloc tile scalars");
+  a.tile_scal = ctx->tile_scal.ptr;
+  a.glob_cnt = ctx->counters + C_SYMV;
+  return DRSDP_OK;
+}
+
+int blk_rowdot(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z, double *zsum) {
+  const Problem &P = ctx->prob;
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  SymvArgs a = base_symv(ctx, (int)P.n, p, T, ldt);
+  a.V = Y;
+  a.ldv = ldv;
+  a.Y = Y;
+  a.ldy = ldv;
+  a.zout = z;
+  a.scal_out = zsum;
+  int rc = blk_tiles(ctx, a);
+  if (rc) return rc;
+  KL(blk_product_launch(a, EPI_ROWDOT, false, (int)P.nblk, (int)P.nb, ctx->stream), "block product (z)");
+  return DRSDP_OK;
+}
+
+// T <- T - sigma (A*(y) - S) on every block (Alg. 2 step 6); scal_out = S_DUAL slots
+int blk_dual(drsdp_ctx *ctx, int p, const double *Y, int ldv, const double *y, double sigma, double *T, int64_t ldt) {
+  const Problem &P = ctx->prob;
+  CK(ctx->red_part.ensure((size_t)blk_elem_blocks((int)P.nblk, (int)P.nb) * 3 + 64), "alloc reduction workspace");
+  BlkElemArgs e;
+  e.t = (int)P.nblk;
+  e.nb = (int)P.nb;
+  e.p = p;
+  e.Y = Y;
+  e.ldy = ldv;
+  e.amap = P.amap.ptr;
+  e.ldm = P.ld;
+  e.y = y;
+  e.T = T;
+  e.ldt = ldt;
+  e.sigma = sigma;
+  e.part = ctx->red_part.ptr;
+  e.counter = ctx->counters + C_DUAL;
+  e.scal_out = ctx->d_scal + S_DUAL;
+  KL(blk_elem_launch(e, BLK_DUAL, ctx->stream), "block dual update");
+  return DRSDP_OK;
+}
+
+static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y,
+                               int ldv, double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost,
+                               double *egrad, double *rgrad);
+static int alm_hvp_blocks(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv,
+                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp);
+
 // y-eliminated subproblem at Y: y(S), M(S) (materialised into Mout), cost/gradients.
 static bool use_dense(const double *Y, const double *U, int ldv) {
   static const bool off = std::getenv("DRSDP_NO_DENSE") != nullptr;
@@ -521,6 +579,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
                  double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost, double *egrad,
                  double *rgrad, double *Dbuf) {
   Problem &P = ctx->prob;
+  if (P.nblk > 0) return alm_costgrad_blocks(ctx, p, T, ldt, sigma, Y, ldv, Mout, ldm, yS, G, rho, cost, egrad, rgrad);
   const int n = (int)P.n;
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
@@ -578,6 +637,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
 int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
             const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf) {
   Problem &P = ctx->prob;
+  if (P.nblk > 0) return alm_hvp_blocks(ctx, p, M, ldm, Y, ldv, U, G, K, rho, wZ, hvp);
   const int n = (int)P.n;
   // K = U^T Y + Y^T U runs on the auxiliary stream, concurrently with Z and its segmented sum
   // (fork / join with events; inside a graph capture this becomes two parallel branches)
@@ -630,6 +690,93 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
   return run_symv(ctx, a, EPI_HVP, true);
 }
 
+
+// Block ALM cost + gradients (oracle/sparse_bqp.py BlockALMProblem.costgrad): G_k, y(S) by the
+// segmented sum over all blocks' positions (global rows), M(S) and the accurate cost sums fused
+// with the S tiles, then the block product with the COSTGRAD row epilogue.
+static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y,
+                               int ldv, double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost,
+                               double *egrad, double *rgrad) {
+  Problem &P = ctx->prob;
+  const int t = (int)P.nblk, nb = (int)P.nb;
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  int rc = ensure_red(ctx, std::max<int64_t>(segsum_blocks(P.m, P.n_large, P.n_huge), blk_elem_blocks(t, nb)), 4);
+  if (rc) return rc;
+  KL(blk_gram_launch(t, nb, p, Y, ldv, nullptr, 0, G, nullptr, ctx->skip_flag, ctx->stream), "block gram");
+  SegArgs s = seg_args(ctx, p, Y, nullptr, ldv, yS);
+  KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
+  BlkElemArgs e;
+  e.t = t;
+  e.nb = nb;
+  e.p = p;
+  e.Y = Y;
+  e.ldy = ldv;
+  e.amap = P.amap.ptr;
+  e.ldm = P.ld;
+  e.y = yS;
+  e.T = const_cast<double *>(T);  // read only in BLK_ASM
+  e.ldt = ldt;
+  e.sigma = sigma;
+  e.M = Mout;
+  e.ldmo = ldm;
+  e.part = ctx->red_part.ptr;
+  e.counter = ctx->counters + C_ASM;
+  e.scal_out = ctx->d_scal + S_ALM;
+  KL(blk_elem_launch(e, BLK_ASM, ctx->stream), "block assembly");
+  KL(alm_cost_launch(ctx->d_scal + S_ALM, sigma, cost ? cost : ctx->d_scal + S_COST, ctx->stream), "alm cost");
+  SymvArgs a = base_symv(ctx, (int)P.n, p, Mout, ldm);
+  a.V = Y;
+  a.ldv = ldv;
+  a.Y = Y;
+  a.ldy = ldv;
+  a.G = G;
+  a.out = rgrad;
+  a.ldo = ldv;
+  a.egrad = egrad;
+  a.lde = ldv;
+  a.rho_out = rho;
+  a.scal_out = ctx->d_scal + S_SCAL;
+  rc = blk_tiles(ctx, a);
+  if (rc) return rc;
+  KL(blk_product_launch(a, EPI_COSTGRAD, false, t, nb, ctx->stream), "block product (cost+grad)");
+  return DRSDP_OK;
+}
+
+// Block ALM HVP (BlockALMProblem.hess): K_k, w = A(Z)/cnt (Z_k = Y_k U_k^T + U_k Y_k^T, segmented
+// sum from Y, U rows), then one block product Q = M U + A*(w) Y (gather) with the HVP epilogue:
+// three launches per Hessian-vector product.
+static int alm_hvp_blocks(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv,
+                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp) {
+  Problem &P = ctx->prob;
+  const int t = (int)P.nblk, nb = (int)P.nb;
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  KL(blk_gram_launch(t, nb, p, Y, ldv, U, ldv, nullptr, K, ctx->skip_flag, ctx->stream), "block gram (K)");
+  SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
+  KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
+  SymvArgs a = base_symv(ctx, (int)P.n, p, M, ldm);
+  a.V = U;
+  a.ldv = ldv;
+  a.amap = P.amap.ptr;
+  a.ldm = P.ld;
+  a.w = wZ;
+  a.X = Y;
+  a.ldx = ldv;
+  a.Y = Y;
+  a.ldy = ldv;
+  a.U = U;
+  a.ldu = ldv;
+  a.G = G;
+  a.K = K;
+  a.rho = rho;
+  a.out = hvp;
+  a.ldo = ldv;
+  a.scal_out = ctx->d_scal + S_SCAL;
+  int rc = blk_tiles(ctx, a);
+  if (rc) return rc;
+  KL(blk_product_launch(a, EPI_HVP, true, t, nb, ctx->stream), "block product (HVP)");
+  return DRSDP_OK;
+}
+
 // ----------------------------------------------------------------------------------------------
 // Problem construction
 // ----------------------------------------------------------------------------------------------
@@ -660,13 +807,18 @@ static int finalize_staged(drsdp_ctx *ctx, Problem &P, const double *C_host) {
   // counts, CSR over upper positions (constraint-major, row-major within a constraint)
   std::vector<int64_t> cnt_upper(m, 0);
   std::vector<int64_t> cnt_ord(m, 0);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t j = i; j < n; ++j) {
-      const int32_t id = P.h_amap[i * n + j];
+  // dense: one n x n block; blocks: row r of block r / nb holds columns [0, nb) of that block
+  const bool blk = P.nblk > 0;
+  const int64_t cols = blk ? P.nb : n;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t base = blk ? r / cols * cols : 0;
+    for (int64_t j = r - base; j < cols; ++j) {
+      const int32_t id = P.h_amap[r * cols + j];
       if (id < 0) continue;
       cnt_upper[id]++;
-      cnt_ord[id] += (i == j) ? 1 : 2;
+      cnt_ord[id] += (r - base == j) ? 1 : 2;
     }
+  }
   for (int64_t a = 0; a < m; ++a)
     if (cnt_ord[a] == 0)
       return set_error(ctx, DRSDP_ERR_SINGULAR_AAT,
@@ -682,12 +834,14 @@ static int finalize_staged(drsdp_ctx *ctx, Problem &P, const double *C_host) {
   P.h_seg_pos.assign(P.n_upper, 0);
   {
     std::vector<int64_t> fill(P.h_seg_ptr.begin(), P.h_seg_ptr.end() - 1);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t j = i; j < n; ++j) {
-        const int32_t id = P.h_amap[i * n + j];
+    for (int64_t r = 0; r < n; ++r) {
+      const int64_t base = blk ? r / cols * cols : 0;
+      for (int64_t j = r - base; j < cols; ++j) {
+        const int32_t id = P.h_amap[r * cols + j];
         if (id < 0) continue;
-        P.h_seg_pos[fill[id]++] = ((uint32_t)i << 16) | (uint32_t)j;
+        P.h_seg_pos[fill[id]++] = ((uint32_t)r << 16) | (uint32_t)(base + j);  // global rows
       }
+    }
   }
   // segment tiers for segsum: <= 32 upper positions one thread, 33..256 one warp, > 256 one block
   std::vector<uint8_t> is_large(m, 0);
@@ -700,9 +854,9 @@ static int finalize_staged(drsdp_ctx *ctx, Problem &P, const double *C_host) {
   P.n_large = (int64_t)large_ids.size();
   P.n_huge = (int64_t)huge_ids.size();
   // device copies
-  P.ld = ((n + 63) / 64) * 64;
+  P.ld = ((cols + 63) / 64) * 64;
   std::vector<int32_t> amap_pad((size_t)n * P.ld, -1);
-  for (int64_t i = 0; i < n; ++i) std::memcpy(&amap_pad[i * P.ld], &P.h_amap[i * n], sizeof(int32_t) * n);
+  for (int64_t i = 0; i < n; ++i) std::memcpy(&amap_pad[i * P.ld], &P.h_amap[i * cols], sizeof(int32_t) * cols);
   CK(P.amap.ensure(amap_pad.size()), "alloc amap");
   CK(cudaMemcpy(P.amap.ptr, amap_pad.data(), sizeof(int32_t) * amap_pad.size(), cudaMemcpyHostToDevice), "copy amap");
   CK(P.cnt.ensure(m), "alloc cnt");
@@ -1014,6 +1168,140 @@ int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c) {
   return finalize_problem(ctx, P, nullptr);
 }
 
+int drsdp_set_blocks(drsdp_ctx *ctx, int32_t nblk, int32_t nb, int64_t m, const int32_t *amaps, const double *b) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  if (nblk < 1 || nb < 1 || (int64_t)nblk * nb >= 65536 || m <= 0 || !amaps || !b)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_blocks: need nblk, nb >= 1, nblk * nb < 65536, m >= 1");
+  const int64_t N = (int64_t)nblk * nb;
+  for (int64_t k = 0; k < nblk; ++k)
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = 0; j < nb; ++j) {
+        const int32_t a = amaps[(k * nb + i) * nb + j];
+        if (a < 0 || a >= m) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_blocks: id out of range");
+        if (a != amaps[(k * nb + j) * nb + i])
+          return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_blocks: block map not symmetric");
+      }
+  cudaSetDevice(ctx->device);
+  Problem P;  // staged
+  P.n = N;
+  P.m = m;
+  P.nblk = nblk;
+  P.nb = nb;
+  P.h_amap.assign(amaps, amaps + N * nb);
+  P.h_b.assign(b, b + m);
+  return finalize_problem(ctx, P, nullptr);
+}
+
+int drsdp_set_bqp_chain(drsdp_ctx *ctx, int32_t q, int32_t t, const double *Q, const double *c) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (ctx->sticky) return ctx->sticky;
+  const int64_t nb = 1 + q + (int64_t)q * (q - 1) / 2;
+  if (q < 2 || t < 1 || !Q || !c || nb * t >= 65536 || (int64_t)(q - 2) * t + 2 > 32767)
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_bqp_chain: need q >= 2, t >= 1, t (1 + q + q(q-1)/2) < 65536");
+  for (int64_t k = 0; k < t; ++k)
+    for (int i = 0; i < q; ++i)
+      for (int j = i + 1; j < q; ++j)
+        if (Q[(k * q + i) * q + j] != Q[(k * q + j) * q + i])
+          return set_error(ctx, DRSDP_ERR_NOT_SYMMETRIC, "set_bqp_chain: Q_k not symmetric");
+  // monomial keys: degree in bits 60.., sorted global indices in 15-bit fields (graded-lex order of
+  // the keys = graded-lex order of sorted index tuples, reading R18)
+  auto key = [](const int *a, int k) {
+    uint64_t v = (uint64_t)k << 60;
+    for (int i = 0; i < k; ++i) v |= (uint64_t)a[i] << (45 - 15 * i);
+    return v;
+  };
+  std::vector<uint64_t> keys;
+  std::vector<int> cl(q);
+  for (int k = 0; k < t; ++k) {
+    for (int i = 0; i < q; ++i) cl[i] = (q - 2) * k + i;  // clique x_k, 0-based
+    int a[4];
+    keys.push_back(key(a, 0));
+    for (int i0 = 0; i0 < q; ++i0) {
+      a[0] = cl[i0];
+      keys.push_back(key(a, 1));
+      for (int i1 = i0 + 1; i1 < q; ++i1) {
+        a[1] = cl[i1];
+        keys.push_back(key(a, 2));
+        for (int i2 = i1 + 1; i2 < q; ++i2) {
+          a[2] = cl[i2];
+          keys.push_back(key(a, 3));
+          for (int i3 = i2 + 1; i3 < q; ++i3) {
+            a[3] = cl[i3];
+            keys.push_back(key(a, 4));
+          }
+        }
+      }
+    }
+  }
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  auto id_of = [&](const int *a, int k) {
+    return (int32_t)(std::lower_bound(keys.begin(), keys.end(), key(a, k)) - keys.begin());
+  };
+  cudaSetDevice(ctx->device);
+  Problem P;  // staged
+  P.nblk = t;
+  P.nb = nb;
+  P.n = nb * t;
+  P.m = (int64_t)keys.size();
+  P.h_amap.assign((size_t)P.n * nb, 0);
+  P.h_b.assign(P.m, 0.0);
+  std::vector<int> bs(nb * 2, -1), bk(nb, 0);
+  for (int k = 0; k < t; ++k) {
+    // block basis v(x_k), graded-lex (P:466 per clique): [], [i], [i, j] over the clique's variables
+    int64_t u = 1;
+    for (int i = 0; i < q; ++i, ++u) {
+      bs[2 * u] = (q - 2) * k + i;
+      bk[u] = 1;
+    }
+    for (int i = 0; i < q; ++i)
+      for (int j = i + 1; j < q; ++j, ++u) {
+        bs[2 * u] = (q - 2) * k + i;
+        bs[2 * u + 1] = (q - 2) * k + j;
+        bk[u] = 2;
+      }
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t j = i; j < nb; ++j) {
+        int a[4], kk = 0, ia = 0, ja = 0;
+        const int *A = &bs[2 * i], *B = &bs[2 * j];
+        const int ka = bk[i], kb = bk[j];
+        while (ia < ka || ja < kb) {  // symmetric difference of two sorted sets
+          if (ja >= kb || (ia < ka && A[ia] < B[ja])) a[kk++] = A[ia++];
+          else if (ia >= ka || B[ja] < A[ia]) a[kk++] = B[ja++];
+          else {
+            ++ia;
+            ++ja;
+          }
+        }
+        const int32_t id = id_of(a, kk);
+        P.h_amap[((size_t)k * nb + i) * nb + j] = id;
+        P.h_amap[((size_t)k * nb + j) * nb + i] = id;
+      }
+    // b: coefficients of x_k^T Q_k x_k + c_k^T x_k mod (x^2 - 1), summed over cliques
+    const double *Qk = Q + (size_t)k * q * q;
+    for (int i = 0; i < q; ++i) P.h_b[0] += Qk[i * q + i];
+    for (int i = 0; i < q; ++i) {
+      int a[1] = {(q - 2) * k + i};
+      P.h_b[id_of(a, 1)] += c[(size_t)k * q + i];
+    }
+    for (int i = 0; i < q; ++i)
+      for (int j = i + 1; j < q; ++j) {
+        int a[2] = {(q - 2) * k + i, (q - 2) * k + j};
+        P.h_b[id_of(a, 2)] += 2.0 * Qk[i * q + j];
+      }
+  }
+  return finalize_problem(ctx, P, nullptr);
+}
+
+int drsdp_get_block_sizes(drsdp_ctx *ctx, int32_t *nblk, int32_t *nb) {
+  if (!ctx) return DRSDP_ERR_INVALID_ARG;
+  if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "no problem set");
+  if (nblk) *nblk = (int32_t)ctx->prob.nblk;
+  if (nb) *nb = (int32_t)(ctx->prob.nblk ? ctx->prob.nb : ctx->prob.n);
+  return DRSDP_OK;
+}
+
 int drsdp_get_sizes(drsdp_ctx *ctx, int64_t *n, int64_t *m, int64_t *n_upper) {
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "no problem set");
@@ -1205,6 +1493,7 @@ int drsdp_assemble_M(drsdp_ctx *ctx, const double *y_dev, const double *T_dev, i
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "assemble_M before set_problem");
   Problem &P = ctx->prob;
+  if (P.nblk > 0) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "assemble_M: dense problems only (fixed-M reading)");
   if (!y_dev || !T_dev || !M_dev || ldt < P.n || ldm < P.n || !(sigma > 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "assemble_M: bad arguments");
   int rc = ensure_red(ctx, 1184, 2);
@@ -1247,13 +1536,18 @@ int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const doub
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "dual_update before set_problem");
   Problem &P = ctx->prob;
-  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !y_dev || !T_dev || ldt < P.n || !z_dev || !scalars_dev)
+  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !y_dev || !T_dev || ldt < (P.nblk ? P.nb : P.n) || !z_dev ||
+      !scalars_dev)
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "dual_update: bad arguments");
   const int n = (int)P.n;
-  int rc = ensure_red(ctx, dual_update_blocks(n), 3);
+  int rc = ensure_red(ctx, std::max(dual_update_blocks(n), P.nblk ? blk_elem_blocks((int)P.nblk, (int)P.nb) : 0), 3);
   if (rc) return rc;
   rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
+  if (P.nblk > 0) {
+    rc = blk_dual(ctx, p, Y_dev, p, y_dev, sigma, T_dev, ldt);
+    if (rc) return rc;
+  } else {
   DualArgs da;
   da.n = n;
   da.p = p;
@@ -1271,6 +1565,7 @@ int drsdp_dual_update(drsdp_ctx *ctx, int32_t p, const double *Y_dev, const doub
   da.counter = ctx->counters + C_DUAL;
   da.scal_out = ctx->d_scal + S_DUAL;
   KL(dual_update_launch(da, ctx->stream), "dual update kernel");
+  }
   rc = rowdot_product(ctx, n, p, T_dev, ldt, Y_dev, p, z_dev, ctx->d_scal + S_ZSUM);
   if (rc) return rc;
   KL(vdot_launch(P.m, y_dev, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY, ctx->stream),
@@ -1294,20 +1589,24 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "alm_eval before set_problem");
   Problem &P = ctx->prob;
-  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !T_dev || ldt < P.n || !(sigma > 0) || (flags & ~3) || !flags)
+  if (p < 1 || p > DRSDP_MAX_P || !Y_dev || !T_dev || ldt < (P.nblk ? P.nb : P.n) || !(sigma > 0) || (flags & ~3) ||
+      !flags)
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: bad arguments");
   if ((flags & DRSDP_EVAL_HVP) && (!U_dev || !hvp_dev))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: HVP needs U and hvp");
   const int n = (int)P.n;
+  const size_t gmul = P.nblk > 0 ? (size_t)P.nblk : 1;  // one G, K per block
+  if (P.nblk > 0 && (p > kBlkMaxP || ldt < P.nb))
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: block problems need p <= 64 and ldt >= nb");
   CK(ctx->alm_M.ensure((size_t)n * P.ld), "alloc M");
   CK(ctx->alm_yS.ensure(P.m), "alloc yS");
   CK(ctx->alm_wZ.ensure(P.m), "alloc wZ");
   CK(ctx->alm_rho.ensure(n), "alloc rho");
-  CK(ctx->alm_G.ensure((size_t)2 * p * p), "alloc G");
-  CK(ctx->alm_K.ensure((size_t)p * p), "alloc K");
+  CK(ctx->alm_G.ensure((size_t)2 * p * p * gmul), "alloc G");
+  CK(ctx->alm_K.ensure((size_t)p * p * gmul), "alloc K");
   int rc;
   if (flags & DRSDP_EVAL_COSTGRAD) {
-    CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
+    if (!P.nblk) CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
     rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->alm_G.ptr,
                       ctx->alm_rho.ptr, cost_dev, egrad_dev, rgrad_dev, ctx->alm_D.ptr);
     if (rc) return rc;
@@ -1321,7 +1620,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
     return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y, T, sigma");
   }
   if (flags & DRSDP_EVAL_HVP) {
-    CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
+    if (!P.nblk) CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
     rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->alm_G.ptr, ctx->alm_K.ptr, ctx->alm_rho.ptr,
                  ctx->alm_wZ.ptr, hvp_dev, ctx->alm_Z.ptr);
     if (rc) return rc;

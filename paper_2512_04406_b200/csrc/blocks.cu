@@ -1,0 +1,314 @@
+// blocks.cu — multi-block (clique-chain) relaxation kernels, SURVEY §8(f) row f2.
+// PAPER.md:434-436 (Algorithm 2 on multi-block SDPs) and P:555-602 (DSDP-sparse): every block
+// S_k = Y_k Y_k^T is an n_b x n_b moment matrix (n_b = 211 at q = 20), the y of a monomial is
+// shared by the blocks it appears in. The blocks are small (t = 120 blocks of 211 rows: 43 MB of
+// M, L2-resident), so the kernels are latency/L2-bound batched operations: one CTA per block or
+// per 16-32-row strip of a block, operands staged in shared memory, FP64 FMA (a 211-wide
+// contraction per output; DMMA fragments would not pay at these sizes). Reductions are fixed-order
+// (bit-reproducible). See blocks.cuh for the stacked layout.
+#include "blocks.cuh"
+#include "common.cuh"
+#include "tile_epilogue.cuh"
+
+namespace drsdp {
+
+// ------------------------------------------------------------------------------------------------
+// per-block Gram (P:239 per block): G_k = Y_k^T Y_k, K_k = U_k^T Y_k + Y_k^T U_k
+// ------------------------------------------------------------------------------------------------
+constexpr int BG_ROWS = 32;
+
+__global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const double *__restrict__ Y, int ldy,
+                                                       const double *__restrict__ U, int ldu, double *__restrict__ G,
+                                                       double *__restrict__ K, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
+  extern __shared__ double sm[];
+  double *ys = sm;
+  double *us = sm + BG_ROWS * p;
+  const int k = blockIdx.x;
+  const int64_t r0 = (int64_t)k * nb;
+  const int pp = p * p;
+  constexpr int MAXO = kBlkMaxP * kBlkMaxP / 256;
+  double g[MAXO], kk[MAXO];
+#pragma unroll
+  for (int q = 0; q < MAXO; ++q) g[q] = kk[q] = 0.0;
+  for (int i0 = 0; i0 < nb; i0 += BG_ROWS) {
+    const int rows = min(BG_ROWS, nb - i0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < rows * p; t += blockDim.x) {
+      const int i = t / p, c = t - i * p;
+      ys[t] = Y[(r0 + i0 + i) * ldy + c];
+      if (U) us[t] = U[(r0 + i0 + i) * ldu + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < MAXO; ++q) {
+      const int o = threadIdx.x + 256 * q;
+      if (o < pp) {
+        const int a = o / p, b = o - a * p;
+        double s = g[q], s2 = kk[q];
+        for (int i = 0; i < rows; ++i) {
+          const double ya = ys[i * p + a], yb = ys[i * p + b];
+          s = fma(ya, yb, s);
+          if (U) s2 = fma(us[i * p + a], yb, fma(ya, us[i * p + b], s2));
+        }
+        g[q] = s;
+        kk[q] = s2;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXO; ++q) {
+    const int o = threadIdx.x + 256 * q;
+    if (o < pp) {
+      if (G) G[(size_t)k * pp + o] = g[q];
+      if (K && U) K[(size_t)k * pp + o] = kk[q];
+    }
+  }
+}
+
+cudaError_t blk_gram_launch(int t, int nb, int p, const double *Y, int ldy, const double *U, int ldu, double *G,
+                            double *K, const int *skip, cudaStream_t st) {
+  if (p > kBlkMaxP) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * BG_ROWS * p * (U ? 2 : 1);
+  blk_gram_kernel<<<t, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip);
+  return cudaGetLastError();
+}
+
+__global__ void blk_gsum_kernel(int t, int p, const double *__restrict__ G, double *__restrict__ out) {
+  const int pp = p * p;
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < pp; o += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < t; ++k) s += G[(size_t)k * pp + o];
+    out[o] = s;
+  }
+}
+
+cudaError_t blk_gsum_launch(int t, int p, const double *G, double *out, cudaStream_t st) {
+  blk_gsum_kernel<<<(p * p + 255) / 256, 256, 0, st>>>(t, p, G, out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------------
+// elementwise block work with S tiles: ALM assembly (M(S) = A*(y(S)) - T/sigma and the accurate
+// cost sums, reading R29) and the dual update (Alg. 2 step 6: T <- T - sigma (A*(y) - S))
+// 32 x 64 tile of one block per CTA; thread (tx, ty) owns column tx and rows ty + 4q (q < 8).
+// ------------------------------------------------------------------------------------------------
+constexpr int BE_R = 32, BE_C = 64, BE_PC = 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) blk_elem_kernel(BlkElemArgs a) {
+  __shared__ double yr[BE_R][BE_PC + 1];
+  __shared__ double yc[BE_C][BE_PC + 1];
+  __shared__ double scratch[64];
+  const int k = blockIdx.z;
+  const int i0 = blockIdx.y * BE_R, j0 = blockIdx.x * BE_C;
+  const int64_t b0 = (int64_t)k * a.nb;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  double s[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+  for (int c0 = 0; c0 < a.p; c0 += BE_PC) {
+    const int pc = min(BE_PC, a.p - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < BE_R * BE_PC; t += 256) {
+      const int i = t / BE_PC, c = t - i * BE_PC;
+      yr[i][c] = (i0 + i < a.nb && c < pc) ? a.Y[(b0 + i0 + i) * a.ldy + c0 + c] : 0.0;
+    }
+    for (int t = threadIdx.x; t < BE_C * BE_PC; t += 256) {
+      const int j = t / BE_PC, c = t - j * BE_PC;
+      yc[j][c] = (j0 + j < a.nb && c < pc) ? a.Y[(b0 + j0 + j) * a.ldy + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < pc; ++c) {
+      const double v = yc[tx][c];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] = fma(yr[ty + 4 * q][c], v, s[q]);
+    }
+  }
+  double v3[3] = {0.0, 0.0, 0.0};
+  const int j = j0 + tx;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i = i0 + ty + 4 * q;
+    if (i < a.nb && j < a.nb) {
+      const int64_t r = b0 + i;
+      const double yv = __ldg(a.y + a.amap[r * a.ldm + j]);
+      const double tv = a.T[r * a.ldt + j];
+      if (MODE == BLK_ASM) {
+        a.M[r * a.ldmo + j] = yv - tv / a.sigma;
+        const double rr = s[q] - yv;
+        v3[0] = fma(rr, rr, v3[0]);
+        v3[1] = fma(tv, s[q], v3[1]);
+        v3[2] = fma(tv, tv, v3[2]);
+      } else {
+        const double rr = yv - s[q];
+        const double tn = tv - a.sigma * rr;
+        a.T[r * a.ldt + j] = tn;
+        v3[0] = fma(rr, rr, v3[0]);
+        v3[1] = fma(tn, tn, v3[1]);
+      }
+    }
+  }
+  grid_sum<3>(v3, a.part, a.counter, a.scal_out, scratch);
+}
+
+int blk_elem_blocks(int t, int nb) { return t * ((nb + BE_R - 1) / BE_R) * ((nb + BE_C - 1) / BE_C); }
+
+cudaError_t blk_elem_launch(const BlkElemArgs &a, int mode, cudaStream_t st) {
+  dim3 grid((a.nb + BE_C - 1) / BE_C, (a.nb + BE_R - 1) / BE_R, a.t);
+  if (mode == BLK_ASM)
+    blk_elem_kernel<BLK_ASM><<<grid, 256, 0, st>>>(a);
+  else
+    blk_elem_kernel<BLK_DUAL><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+__global__ void blk_initd_kernel(int64_t total, int nb, const int32_t *__restrict__ amap, int64_t ldm,
+                                 const double *__restrict__ b, const int32_t *__restrict__ cnt, double *__restrict__ T,
+                                 int64_t ldt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nb;
+    const int j = (int)(e - r * nb);
+    const int32_t id = amap[r * ldm + j];
+    T[r * ldt + j] = b[id] / (double)cnt[id];
+  }
+}
+
+cudaError_t blk_initd_launch(int t, int nb, const int32_t *amap, int64_t ldm, const double *b, const int32_t *cnt,
+                             double *T, int64_t ldt, cudaStream_t st) {
+  const int64_t total = (int64_t)t * nb * nb;
+  blk_initd_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(total, nb, amap, ldm, b,
+                                                                                          cnt, T, ldt);
+  return cudaGetLastError();
+}
+
+__global__ void blk_makex_kernel(int64_t total, int nb, const double *__restrict__ T, int64_t ldt,
+                                 const double *__restrict__ z, double *__restrict__ X) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nb;  // global row = k nb + i
+    const int j = (int)(e - r * nb);
+    const int i = (int)(r % nb);
+    // column-major block k: element (i, j) at X[k nb^2 + j nb + i]; X symmetric, so the row-major
+    // element index e = (k nb + i) nb + j addresses element (j, i) = (i, j)
+    X[e] = T[r * ldt + j] - (i == j ? z[r] : 0.0);
+  }
+}
+
+cudaError_t blk_makex_launch(int t, int nb, const double *T, int64_t ldt, const double *z, double *X, cudaStream_t st) {
+  const int64_t total = (int64_t)t * nb * nb;
+  blk_makex_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(total, nb, T, ldt, z, X);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------------
+// block-diagonal product + row epilogue
+// ------------------------------------------------------------------------------------------------
+constexpr int BP_R = 16, BP_J = 32;
+
+template <int PT, int EPI, bool GATHER>
+__global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, int nstrip) {
+  if (a.skip && *(volatile const int *)a.skip) return;
+  extern __shared__ double sm[];
+  constexpr bool NEEDG = EPI == EPI_COSTGRAD || EPI == EPI_HVP;
+  const int p = a.p;
+  double *gs = sm;                                        // 2 p^2 (G, K)
+  double *ptile = gs + (NEEDG ? 2 * p * p : 0);           // BP_R x PT
+  double *As = ptile + BP_R * PT;                         // BP_R x (BP_J + 1)
+  double *Vs = As + BP_R * (BP_J + 1);                    // BP_J x PT
+  double *Ws = Vs + BP_J * PT;                            // BP_R x (BP_J + 1) (gather)
+  double *Xs = Ws + (GATHER ? BP_R * (BP_J + 1) : 0);     // BP_J x PT (gather)
+  __shared__ double scratch[64];
+  __shared__ unsigned s_ticket;
+  const int tile = blockIdx.x;
+  const int k = tile / nstrip, st = tile - k * nstrip;
+  const int64_t b0 = (int64_t)k * nb;
+  const int li0 = st * BP_R;
+  const int rows = min(BP_R, nb - li0);
+  const int64_t r0 = b0 + li0;
+  constexpr int QN = BP_R * PT / 256 > 0 ? BP_R * PT / 256 : 1;
+  double acc[QN];
+#pragma unroll
+  for (int q = 0; q < QN; ++q) acc[q] = 0.0;
+  for (int j0 = 0; j0 < nb; j0 += BP_J) {
+    const int jn = min(BP_J, nb - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < BP_R * BP_J; e += 256) {
+      const int i = e / BP_J, jj = e - i * BP_J;
+      const bool ok = i < rows && jj < jn;
+      As[i * (BP_J + 1) + jj] = ok ? a.A[(r0 + i) * a.lda + j0 + jj] : 0.0;
+      if constexpr (GATHER) Ws[i * (BP_J + 1) + jj] = ok ? __ldg(a.w + a.amap[(r0 + i) * a.ldm + j0 + jj]) : 0.0;
+    }
+    for (int e = threadIdx.x; e < BP_J * PT; e += 256) {
+      const int jj = e / PT, c = e - jj * PT;
+      const bool ok = jj < jn && c < p;
+      Vs[e] = ok ? a.V[(b0 + j0 + jj) * a.ldv + c] : 0.0;
+      if constexpr (GATHER) Xs[e] = ok ? a.X[(b0 + j0 + jj) * a.ldx + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      const int o = threadIdx.x + 256 * q;
+      if (o < BP_R * PT) {
+        const int i = o / PT, c = o - i * PT;
+        double s = acc[q];
+        for (int jj = 0; jj < jn; ++jj) {
+          s = fma(As[i * (BP_J + 1) + jj], Vs[jj * PT + c], s);
+          if constexpr (GATHER) s = fma(Ws[i * (BP_J + 1) + jj], Xs[jj * PT + c], s);
+        }
+        acc[q] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < QN; ++q) {
+    const int o = threadIdx.x + 256 * q;
+    if (o < BP_R * PT) ptile[o] = acc[q];
+  }
+  SymvArgs al = a;
+  if constexpr (NEEDG) {
+    al.G = a.G + (size_t)k * p * p;
+    if (a.K) al.K = a.K + (size_t)k * p * p;
+  }
+  __syncthreads();
+  tile_epilogue<PT, EPI, BP_R, 256>(al, ptile, gs, scratch, &s_ticket, tile, (int)r0, 0, (int)(b0 + nb), p);
+}
+
+int blk_product_tiles(int t, int nb) { return t * ((nb + BP_R - 1) / BP_R); }
+
+template <int PT, int EPI, bool GATHER>
+static cudaError_t launch_bp(const SymvArgs &a, int t, int nb, cudaStream_t st) {
+  constexpr bool NEEDG = EPI == EPI_COSTGRAD || EPI == EPI_HVP;
+  const int nstrip = (nb + BP_R - 1) / BP_R;
+  const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * (BP_J + 1) + BP_J * PT +
+                                        (GATHER ? BP_R * (BP_J + 1) + BP_J * PT : 0));
+  auto kern = blk_product_kernel<PT, EPI, GATHER>;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<t * nstrip, 256, smem, st>>>(a, nb, nstrip);
+  return cudaGetLastError();
+}
+
+template <int PT>
+static cudaError_t launch_bp_pt(const SymvArgs &a, int epi, bool gather, int t, int nb, cudaStream_t st) {
+  switch (epi) {
+    case EPI_COSTGRAD:
+      return launch_bp<PT, EPI_COSTGRAD, false>(a, t, nb, st);
+    case EPI_HVP:
+      return gather ? launch_bp<PT, EPI_HVP, true>(a, t, nb, st) : launch_bp<PT, EPI_HVP, false>(a, t, nb, st);
+    case EPI_ROWDOT:
+      return launch_bp<PT, EPI_ROWDOT, false>(a, t, nb, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t blk_product_launch(const SymvArgs &a, int epi, bool gather, int t, int nb, cudaStream_t st) {
+  if (a.p <= 16) return launch_bp_pt<16>(a, epi, gather, t, nb, st);
+  if (a.p <= 32) return launch_bp_pt<32>(a, epi, gather, t, nb, st);
+  if (a.p <= 64) return launch_bp_pt<64>(a, epi, gather, t, nb, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace drsdp

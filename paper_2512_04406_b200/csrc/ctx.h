@@ -73,8 +73,12 @@ enum Counter { C_GRAM = 0, C_SEG, C_ASM, C_DUAL, C_VEC, C_SYMV, C_FRO, C_DOT, C_
 
 struct Problem {
   int64_t n = 0, m = 0, ld = 0, n_upper = 0;
+  // multi-block problem (blocks.cuh): nblk blocks of nb rows, n = nblk * nb rows of
+  // the factor; h_amap / amap / T / M are stacked (row r at r * nb / r * ld, nb columns).
+  // nblk = 0: one dense n x n block.
+  int64_t nblk = 0, nb = 0;
   bool has_C = false;
-  std::vector<int32_t> h_amap;  // n*n, -1 = unconstrained
+  std::vector<int32_t> h_amap;  // n*n (dense; -1 = unconstrained) or n*nb (blocks)
   std::vector<int64_t> h_seg_ptr;
   std::vector<uint32_t> h_seg_pos;
   std::vector<int32_t> h_cnt;
@@ -204,5 +208,8 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
 int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
             const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf);
 int read_scalars(drsdp_ctx *ctx, int first, int count);
+// multi-block problems (blocks.cu): z = rowdot(T Y, Y) per block and the per-block dual update
+int blk_rowdot(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z, double *zsum);
+int blk_dual(drsdp_ctx *ctx, int p, const double *Y, int ldv, const double *y, double sigma, double *T, int64_t ldt);
 void free_solver(drsdp_ctx *ctx);
 }  // namespace drsdp

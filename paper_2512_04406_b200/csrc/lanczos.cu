@@ -361,6 +361,7 @@ extern "C" int drsdp_x_eigs(drsdp_ctx *ctx, const double *T_dev, int64_t ldt, co
   if (!ctx) return DRSDP_ERR_INVALID_ARG;
   if (ctx->sticky) return ctx->sticky;
   if (!ctx->has_problem) return set_error(ctx, DRSDP_ERR_STATE, "x_eigs before set_problem");
+  if (ctx->prob.nblk > 0) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "x_eigs: dense problems only");
   const int n = (int)ctx->prob.n;
   if (!T_dev || !z_dev || ldt < n || steps < 1 || nvec < 0 || nvec > n || (nvec > 0 && (!ritz || !V_dev)))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "x_eigs: bad arguments");

@@ -20,6 +20,7 @@
 #include "ctx.h"
 #include "kernels.cuh"
 #include "lanczos.cuh"
+#include "blocks.cuh"
 #include "symv.cuh"
 
 namespace drsdp {
@@ -70,6 +71,11 @@ struct SolverState {
   } graphs[2];
   cudaStream_t priv = nullptr;   // private capture-capable stream used for the whole solve
   cusolverDnHandle_t sol = nullptr;
+  // multi-block problems: batched eigen step (cusolverDnXsyevBatched) workspaces
+  cusolverDnParams_t sparams = nullptr;
+  size_t bwork_dev = 0;
+  std::vector<char> bwork_host;
+  DBuf<int> binfo;
   Point cur, prop;
   int p = 0;
   bool have_solution = false;
@@ -100,6 +106,8 @@ void free_solver(drsdp_ctx *ctx) {
   for (auto &g : s->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (s->priv) cudaStreamDestroy(s->priv);
+  s->binfo.release();
+  if (s->sparams) cusolverDnDestroyParams(s->sparams);
   if (s->sol) cusolverDnDestroy(s->sol);
   delete s;
   ctx->solver = nullptr;
@@ -226,7 +234,11 @@ struct Run {
 
   // reading R35: precond_mu < 0 selects mu = 0.1 for n >= 2048 (measured: d = 80 twice as fast,
   // d = 40 slower with it) and no preconditioner below
-  double mu() const { return prm.precond_mu >= 0.0 ? prm.precond_mu : (n >= 2048 ? 0.1 : 0.0); }
+  // block problems: off (reading R37; the Gram of one block is not the operator of the others)
+  double mu() const {
+    if (ctx->prob.nblk > 0) return 0.0;
+    return prm.precond_mu >= 0.0 ? prm.precond_mu : (n >= 2048 ? 0.1 : 0.0);
+  }
   bool precond() const { return mu() > 0.0; }
   // W = gbar (G + mu gbar I)^{-1} at the current point: A = G/gbar + mu I (kernel), Cholesky
   // A = L L^T and W = A^{-1} by potrs on the identity (cuSOLVER, p x p); info checked with the
@@ -461,12 +473,13 @@ static int set_pitch(drsdp_ctx *ctx, int ldp_new, bool keep_cur, int p) {
     if (!(keep_cur && b == &s->Ybuf[0])) CK(b->ensure(nv), "alloc factor-sized vectors");
   if (keep_cur) std::swap(s->Ybuf[0], keep);
   const size_t pp = (size_t)ldp_new * ldp_new;
-  for (int k = 0; k < 2; ++k) CK(s->Gbuf[k].ensure(pp), "alloc G");
-  CK(s->K.ensure(pp), "alloc K");
+  const size_t gmul = ctx->prob.nblk > 0 ? (size_t)ctx->prob.nblk : 1;  // block problems: one G, K per block
+  for (int k = 0; k < 2; ++k) CK(s->Gbuf[k].ensure(pp * gmul), "alloc G");
+  CK(s->K.ensure(pp * gmul), "alloc K");
   CK(s->Wsmall.ensure(pp), "alloc W");
   CK(s->Geig.ensure(pp), "alloc");
   CK(s->Gw.ensure(ldp_new), "alloc");
-  CK(ctx->g_scratch.ensure(2 * pp), "alloc G");
+  CK(ctx->g_scratch.ensure(2 * pp * gmul), "alloc G");
   int lw = 0;
   if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, ldp_new, s->Geig.ptr,
                                   ldp_new, s->Gw.ptr, &lw) != CUSOLVER_STATUS_SUCCESS)
@@ -499,14 +512,14 @@ static int alloc_solver(drsdp_ctx *ctx, int p0) {
     CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
     CK(s->rhobuf[k].ensure(P.n), "alloc");
     CK(s->ySbuf[k].ensure(P.m), "alloc");
-    if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Dbuf[k].ensure((size_t)P.n * P.ld), "alloc dense S");
+    if (std::getenv("DRSDP_NO_DENSE") == nullptr && !P.nblk) CK(s->Dbuf[k].ensure((size_t)P.n * P.ld), "alloc dense S");
   }
-  if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Zbuf.ensure((size_t)P.n * P.ld), "alloc dense Z");
+  if (std::getenv("DRSDP_NO_DENSE") == nullptr && !P.nblk) CK(s->Zbuf.ensure((size_t)P.n * P.ld), "alloc dense Z");
   s->ldp = 0;
   RC(set_pitch(ctx, std::max(64, ((p0 + 63) / 64) * 64), false, 0));
   CK(s->wZ.ensure(P.m), "alloc");
   CK(s->T.ensure((size_t)P.n * P.ld), "alloc T");
-  CK(s->X.ensure((size_t)P.n * P.n), "alloc X");
+  CK(s->X.ensure(P.nblk ? (size_t)P.n * P.nb : (size_t)P.n * P.n), "alloc X");
   CK(s->W.ensure(P.n), "alloc W");
   CK(s->ystar.ensure(P.m), "alloc");
   CK(s->z.ensure(P.n), "alloc");
@@ -515,9 +528,25 @@ static int alloc_solver(drsdp_ctx *ctx, int p0) {
   if (!s->h_tcg) CK(cudaMallocHost(&s->h_tcg, sizeof(TcgDev)), "alloc pinned");
   CK(s->Vst.ensure((size_t)P.n * std::max(1, ctx->prm.escape_max)), "alloc escape vectors");
   CK(ctx->red_part.ensure((size_t)std::max<int64_t>({(int64_t)segsum_blocks(P.m, P.n_large, P.n_huge),
-                                                     (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184}) *
+                                                     (int64_t)dual_update_blocks((int)P.n), rows_blocks(P.n), 1184,
+                                                     P.nblk ? (int64_t)blk_elem_blocks((int)P.nblk, (int)P.nb) : 0}) *
                               4 + 64),
      "alloc red");
+  if (P.nblk > 0) {
+    // batched eigen step over the blocks (X_k = T_k - Diag z_k, column-major, contiguous)
+    if (!s->sparams && cusolverDnCreateParams(&s->sparams) != CUSOLVER_STATUS_SUCCESS)
+      return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnCreateParams");
+    size_t dbytes = 0, hbytes = 0;
+    if (cusolverDnXsyevBatched_bufferSize(s->sol, s->sparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, P.nb,
+                                          CUDA_R_64F, s->X.ptr, P.nb, CUDA_R_64F, s->W.ptr, CUDA_R_64F, &dbytes, &hbytes,
+                                          P.nblk) != CUSOLVER_STATUS_SUCCESS)
+      return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnXsyevBatched_bufferSize");
+    CK(s->work.ensure(dbytes / sizeof(double) + 2), "alloc batched eig workspace");
+    s->bwork_dev = dbytes;
+    s->bwork_host.resize(hbytes + 1);
+    CK(s->binfo.ensure((size_t)P.nblk), "alloc info");
+    return DRSDP_OK;
+  }
   int lwork = 0;
   if (cusolverDnDsyevd_bufferSize(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)P.n, s->X.ptr,
                                   (int)P.n, s->W.ptr, &lwork) != CUSOLVER_STATUS_SUCCESS)
@@ -588,6 +617,12 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   if (ctx->p0_given && ctx->h_Y0.size() != (size_t)ctx->prob.n * ctx->p0_given)
     return set_error(ctx, DRSDP_ERR_STATE, "initial factor does not match the problem size");
   int p = ctx->p0_given ? ctx->p0_given : prm.p0;
+  const bool blocks = ctx->prob.nblk > 0;
+  const int nblk = (int)ctx->prob.nblk, nbk = (int)ctx->prob.nb;
+  // rank cap: p <= n (S has rank <= n); block problems: p <= min(64, n_b) (blocks.cuh)
+  const int pcap = blocks ? std::min(kBlkMaxP, nbk) : std::min<int>(DRSDP_MAX_P, (int)ctx->prob.n);
+  if (blocks && prm.mode == 1) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems: ALM mode only");
+  if (blocks && p > pcap) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems: p0 <= min(64, n_b)");
   RC(alloc_solver(ctx, p));
   SolverState *s = ctx->solver;
   Problem &P = ctx->prob;
@@ -608,7 +643,10 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     CK(cudaStreamSynchronize(ctx->stream), "sync");
   }
   // T^0 = D = A*(b/cnt) (X~^0 = 0), y^0 = 0
-  KL(init_d_launch(n, P.amap.ptr, P.ld, P.b.ptr, P.cnt.ptr, s->T.ptr, P.ld, ctx->stream), "init D");
+  if (blocks)
+    KL(blk_initd_launch(nblk, nbk, P.amap.ptr, P.ld, P.b.ptr, P.cnt.ptr, s->T.ptr, P.ld, ctx->stream), "init D");
+  else
+    KL(init_d_launch(n, P.amap.ptr, P.ld, P.b.ptr, P.cnt.ptr, s->T.ptr, P.ld, ctx->stream), "init D");
   CK(cudaMemsetAsync(s->ystar.ptr, 0, sizeof(double) * P.m, ctx->stream), "memset y");
   double b_norm = 0.0;
   for (double v : P.h_b) b_norm += v * v;
@@ -703,7 +741,10 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     da.part = ctx->red_part.ptr;
     da.counter = ctx->counters + C_DUAL;
     da.scal_out = ctx->d_scal + S_DUAL;
-    KL(dual_update_launch(da, ctx->stream), "dual update");
+    if (blocks)
+      RC(blk_dual(ctx, p, s->cur.Y, s->ldp, s->ystar.ptr, run.sigma, s->T.ptr, P.ld));
+    else
+      KL(dual_update_launch(da, ctx->stream), "dual update");
     // z = rowdot(T Y, Y)
     RC(rowdot_product(ctx, n, p, s->T.ptr, P.ld, s->cur.Y, s->ldp, s->z.ptr, ctx->d_scal + S_ZSUM));
     KL(vdot_launch(P.m, s->ystar.ptr, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY,
@@ -722,7 +763,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     eta_g = std::fabs(dobj - pobj) / (1.0 + std::fabs(dobj) + std::fabs(pobj));
     // auto: dense below n = 16384 (measured at d = 80: Lanczos escape directions cost 162 outer
     // iterations / 65 s against 29 / 21 s with dsyevd; reading R17)
-    const bool lanczos = prm.eig_method == 2 || (prm.eig_method == 0 && n >= 16384);
+    const bool lanczos = !blocks && (prm.eig_method == 2 || (prm.eig_method == 0 && n >= 16384));
     const int nvec = std::max(1, std::min(prm.escape_max, n));
     int nlam = 0;                   // smallest eigen/Ritz values available in lam[0..nlam)
     double lam_top = 0.0;           // largest eigen/Ritz value
@@ -748,7 +789,45 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       dense_done = true;
       return DRSDP_OK;
     };
-    if (lanczos) {
+    // block problems: the spectrum of the block-diagonal X is the union of the blocks' spectra
+    // (reading R38); all blocks in one batched decomposition, merged on the host in ascending
+    // order (ties: lower block, then lower index first), escape vectors embedded in their rows
+    std::vector<std::pair<int, int>> blk_src;  // (block, eigen index) of lam[i]
+    auto block_eig = [&]() -> int {
+      KL(blk_makex_launch(nblk, nbk, s->T.ptr, P.ld, s->z.ptr, s->X.ptr, ctx->stream), "make X (blocks)");
+      if (cusolverDnXsyevBatched(s->sol, s->sparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, nbk, CUDA_R_64F,
+                                 s->X.ptr, nbk, CUDA_R_64F, s->W.ptr, CUDA_R_64F, s->work.ptr, s->bwork_dev,
+                                 s->bwork_host.data(), s->bwork_host.size() - 1, s->binfo.ptr,
+                                 nblk) != CUSOLVER_STATUS_SUCCESS)
+        return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnXsyevBatched");
+      ctx->launches++;
+      std::vector<double> wb((size_t)n);
+      std::vector<int> infos(nblk);
+      CK(cudaMemcpyAsync(wb.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
+      CK(cudaMemcpyAsync(infos.data(), s->binfo.ptr, sizeof(int) * nblk, cudaMemcpyDeviceToHost, ctx->stream),
+         "read info");
+      CK(cudaStreamSynchronize(ctx->stream), "sync");
+      for (int k2 = 0; k2 < nblk; ++k2)
+        if (infos[k2] != 0)
+          return set_error(ctx, DRSDP_ERR_NUMERIC, "batched eigen-decomposition failed (block " + std::to_string(k2) + ")");
+      std::vector<std::pair<double, std::pair<int, int>>> all((size_t)n);
+      for (int k2 = 0; k2 < nblk; ++k2)
+        for (int i = 0; i < nbk; ++i) all[(size_t)k2 * nbk + i] = {wb[(size_t)k2 * nbk + i], {k2, i}};
+      std::sort(all.begin(), all.end());
+      blk_src.resize(n);
+      for (int i = 0; i < n; ++i) {
+        lam[i] = all[i].first;
+        blk_src[i] = all[i].second;
+      }
+      nlam = n;
+      lam_top = lam[n - 1];
+      vec_cols = nullptr;
+      dense_done = true;
+      return DRSDP_OK;
+    };
+    if (blocks) {
+      RC(block_eig());
+    } else if (lanczos) {
       const int b = std::min(16, n);
       const int kmax = std::max(1, std::min(prm.lanczos_steps > 0 ? prm.lanczos_steps : 40, n / b));
       if (s->lz.n != n || s->lz.b != b || s->lz.kmax != kmax) {
@@ -797,7 +876,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam_top));
     int dv = 0;
     while (dv < prm.escape_max && dv < nlam && dv < (dense_done ? n : nvec) && lam[dv] < thresh) ++dv;
-    if (dv > 0 && p + dv > std::min(DRSDP_MAX_P, n)) dv = std::max(0, std::min(DRSDP_MAX_P, n) - p);
+    if (dv > 0 && p + dv > pcap) dv = std::max(0, pcap - p);
     // escape gate (reading R36): the certificate X^{k+1} is the subproblem's (Prop 4.3) only at a
     // stationary point; while the inner solve ends far above its tolerance, keep the rank (no escape,
     // no reduction)
@@ -808,8 +887,11 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     // Eigenpairs of the p x p Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so
     // row/column-major agree).
     if (dv == 0 && !gated) {
-      CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
-         "copy G");
+      if (blocks)
+        KL(blk_gsum_launch(nblk, p, s->cur.G, s->Geig.ptr, ctx->stream), "sum block Gram");  // Y^T Y = sum_k G_k
+      else
+        CK(cudaMemcpyAsync(s->Geig.ptr, s->cur.G, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, ctx->stream),
+           "copy G");
       const int lw = (int)s->gwork.cap - 1;
       if (cusolverDnDsyevd(s->sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, p, s->Geig.ptr, p, s->Gw.ptr,
                            s->gwork.ptr, lw, s->devinfo.ptr) != CUSOLVER_STATUS_SUCCESS)
@@ -845,9 +927,19 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     if (dv > 0) {
       if (p + dv > s->ldp) RC(set_pitch(ctx, ((p + dv + 63) / 64) * 64, true, p));
       // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]
-      std::vector<double> Vh((size_t)n * dv);
-      CK(cudaMemcpyAsync(Vh.data(), vec_cols, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
-         "read V");
+      std::vector<double> Vh((size_t)n * dv, 0.0);
+      if (blocks) {
+        // eigenvector i of block k (column i of the column-major X_k) into rows k n_b .. of column c
+        for (int c = 0; c < dv; ++c) {
+          const int kb = blk_src[c].first, ib = blk_src[c].second;
+          CK(cudaMemcpyAsync(Vh.data() + (size_t)c * n + (size_t)kb * nbk, s->X.ptr + ((size_t)kb * nbk + ib) * nbk,
+                             sizeof(double) * nbk, cudaMemcpyDeviceToHost, ctx->stream),
+             "read V");
+        }
+      } else {
+        CK(cudaMemcpyAsync(Vh.data(), vec_cols, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
+           "read V");
+      }
       CK(cudaStreamSynchronize(ctx->stream), "sync");
       for (int c = 0; c < dv; ++c) {
         int km = 0;
@@ -918,8 +1010,14 @@ extern "C" int drsdp_get_solution(drsdp_ctx *ctx, double *y, double *Y, int32_t 
        "read Y");
   if (z) CK(cudaMemcpyAsync(z, s->z.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read z");
   if (X) {
-    KL(make_x_launch((int)n, s->T.ptr, s->ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
-    CK(cudaMemcpyAsync(X, s->X.ptr, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream), "read X");
+    const Problem &P = ctx->prob;
+    if (P.nblk > 0) {
+      KL(blk_makex_launch((int)P.nblk, (int)P.nb, s->T.ptr, s->ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
+      CK(cudaMemcpyAsync(X, s->X.ptr, sizeof(double) * n * P.nb, cudaMemcpyDeviceToHost, ctx->stream), "read X");
+    } else {
+      KL(make_x_launch((int)n, s->T.ptr, s->ld, s->z.ptr, s->X.ptr, ctx->stream), "make X");
+      CK(cudaMemcpyAsync(X, s->X.ptr, sizeof(double) * n * n, cudaMemcpyDeviceToHost, ctx->stream), "read X");
+    }
   }
   CK(cudaStreamSynchronize(ctx->stream), "sync");
   return DRSDP_OK;

@@ -3,7 +3,8 @@
 many calls, to show where solve time goes. Synthetic state: T symmetric N(0, 1/n), unit-row
 Y, tangent U (the parity tests check these calls against the oracle).
 
-Usage: python tools/alm_profile.py [d] [p,p,...] [reps]
+Usage: python tools/alm_profile.py [d | chain:q:t] [p,p,...] [reps]
+  chain:q:t times the multi-block evaluation of the clique-chain relaxation (blocks.cu)
 """
 import sys
 import time
@@ -15,19 +16,34 @@ sys.path.insert(0, ".")
 from inputs import bqp_instance  # noqa: E402
 from paper_2512_04406_b200 import abi  # noqa: E402
 
-d = int(sys.argv[1]) if len(sys.argv) > 1 else 80
+arg = sys.argv[1] if len(sys.argv) > 1 else "80"
 ps = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [16, 64, 128, 240]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 50
 ctx = abi.Context(0, 0)
-Q, c = bqp_instance(d, 0)
-ctx.set_bqp(Q, c)
-n = ctx.sizes()[0]
-ld = n + (-n) % 64
 rng = np.random.default_rng(0)
-T = rng.standard_normal((n, n)) / np.sqrt(n)
-T = (T + T.T) / 2
-Tp = np.zeros((n, ld))
-Tp[:, :n] = T
+if arg.startswith("chain"):
+    from inputs import chain_bqp_instance  # noqa: E402
+
+    _, q, t = arg.split(":")
+    ctx.set_bqp_chain(*chain_bqp_instance(int(q), int(t), 0))
+    d = arg
+    n = ctx.sizes()[0]
+    nb = ctx.block_sizes()[1]
+    ld = nb + (-nb) % 64
+    Tp = np.zeros((n, ld))
+    for k in range(int(t)):
+        B = rng.standard_normal((nb, nb)) / np.sqrt(nb)
+        Tp[k * nb:(k + 1) * nb, :nb] = (B + B.T) / 2
+else:
+    d = int(arg)
+    Q, c = bqp_instance(d, 0)
+    ctx.set_bqp(Q, c)
+    n = ctx.sizes()[0]
+    ld = n + (-n) % 64
+    T = rng.standard_normal((n, n)) / np.sqrt(n)
+    T = (T + T.T) / 2
+    Tp = np.zeros((n, ld))
+    Tp[:, :n] = T
 Td = torch.from_numpy(Tp).cuda()
 for p in ps:
     Y = rng.standard_normal((n, p))

@@ -62,5 +62,31 @@ for graph in (False, True):
     ctx.set_initial_factor(initial_factor(n, 2, 0))
     info = ctx.solve()
     print("solve", graph, info["status"], info["dual_obj"], flush=True)
+# multi-block (clique-chain) relaxation: block evaluations and a small solve (blocks.cu)
+from inputs import chain_bqp_instance  # noqa: E402
+
+Qs, cs = chain_bqp_instance(6, 3, 0)
+ctx.set_bqp_chain(Qs, cs)
+n = ctx.sizes()[0]
+t, nb = ctx.block_sizes()
+ld = nb + (-nb) % 64
+Tb = np.zeros((n, ld))
+Tb[:, :nb] = 0.1 * np.random.default_rng(3).standard_normal((n, nb))
+for k in range(t):
+    blk = Tb[k * nb:(k + 1) * nb, :nb]
+    Tb[k * nb:(k + 1) * nb, :nb] = blk + blk.T
+Td = dev(Tb)
+for p in (3, 20):
+    Y, U = sweep_factor(n, p)
+    Yd, Ud = dev(Y), dev(U)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    R, H = torch.empty_like(Yd), torch.empty_like(Yd)
+    ctx.alm_eval(abi.EVAL_COSTGRAD | abi.EVAL_HVP, p, Td, ld, 2.0, Yd, Ud, cost, None, R, H)
+    ctx.sync()
+    print("block alm", n, p, cost.item(), flush=True)
+ctx.set_params(ctx.default_params(p0=2))
+ctx.set_initial_factor(initial_factor(n, 2, 0))
+info = ctx.solve()
+print("block solve", info["status"], info["dual_obj"], flush=True)
 ctx.close()
 print("SANITIZE_CASES_DONE")
