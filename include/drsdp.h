@@ -158,8 +158,8 @@ typedef struct {
   uint64_t seed;                       /* Y^0 draw when no initial factor is given                */
   double rho_reg;                      /* trust-region ratio regularisation: max(1,|f|) eps rho_reg (R12) */
   int32_t stall_rtr;                   /* stagnation: stop RTR when ||grad|| has not halved within
-                                          stall_rtr iterations and is within 100x of the inner
-                                          tolerance (0 = never; reading R30)                       */
+                                          stall_rtr iterations and is within stall_factor x the
+                                          inner tolerance (0 = never; reading R30)                       */
   int32_t eig_method;                  /* eigen step (eta_d, escape directions): 0 = auto (block
                                           Lanczos for n >= 16384, dense dsyevd below), 1 = dense dsyevd
                                           every outer iteration, 2 = block Lanczos always. With
@@ -174,6 +174,8 @@ typedef struct {
   double escape_gate;                  /* escape / rank change only when the inner solve ended with
                                           ||grad|| <= escape_gate x its tolerance (reading R36);
                                           0 = always                                               */
+  double stall_factor;                 /* the stagnation exit (stall_rtr) applies only within
+                                          stall_factor x the inner tolerance (reading R30; default 100) */
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);

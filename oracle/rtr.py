@@ -93,7 +93,7 @@ def tcg(prob, ctx, Y, g, Delta, prm: RTRParams, prec=None):
     return eta, Heta, j, hit
 
 
-def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, stall=0):
+def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, stall=0, stall_factor=100.0):
     """Minimise prob over the oblique manifold from Y. Returns (Y, info dict).
 
     warm_U: optional second-order descent direction (Thm 4.5); a curvilinear
@@ -128,7 +128,7 @@ def rtr(prob, Y, prm: RTRParams, grad_tol: float, warm_U=None, max_halvings=25, 
             best_gn, since_best = gn, 0
         else:
             since_best += 1
-            if stall > 0 and since_best > stall and gn <= 100.0 * grad_tol:
+            if stall > 0 and since_best > stall and gn <= stall_factor * grad_tol:
                 break
         info["iters"] += 1
         eta, Heta, nin, hit = tcg(prob, ctx, Y, g, Delta, prm, gram_preconditioner(Y, prm.precond_mu))

@@ -285,7 +285,7 @@ def solve_blocks(amaps, cnt, b, prm: Params, Y0: np.ndarray, verbose=False):
         Y, info = rtr(prob, Y, RTRParams(N, p, max_iter=prm.max_rtr, rho_reg=prm.rho_reg,
                                         max_tcg=prm.max_tcg if prm.max_tcg > 0 else None,
                                         precond_mu=0.0), grad_tol, warm_U=U,
-                      stall=prm.stall_rtr)
+                      stall=prm.stall_rtr, stall_factor=prm.stall_factor)
         totals["rtr"] += info["iters"]
         totals["tcg"] += info["tcg"]
         totals["costgrad"] += prob.n_costgrad

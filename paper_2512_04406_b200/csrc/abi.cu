@@ -1346,6 +1346,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->rho_reg = 1e3;
   o->stall_rtr = 10;
   o->precond_mu = -1.0;  // auto (reading R35)
+  o->stall_factor = 100.0;
   o->escape_gate = 0.0;
   return DRSDP_OK;
 }
@@ -1356,7 +1357,7 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
   if (!(q.sigma0 > 0 && q.sigma_min > 0 && q.sigma_max > q.sigma_min && q.gamma > 1 && q.tau1 > 0 &&
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
-        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
+        q.rho_reg >= 0 && q.stall_rtr >= 0 && q.stall_factor > 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
         q.escape_gate >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;

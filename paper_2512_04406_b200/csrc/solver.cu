@@ -365,7 +365,7 @@ struct Run {
     iters_out = 0;
     tcg_out = 0;
     // stagnation exit (reading R30): stop when the gradient norm has not halved within the last
-    // stall_rtr trust-region iterations and is within 100x of the tolerance
+    // stall_rtr trust-region iterations and is within stall_factor (100) x the tolerance
     double best_gn = s->cur.gn;
     int since_best = 0;
     for (int it = 0; it < prm.max_rtr; ++it) {
@@ -376,7 +376,7 @@ struct Run {
       if (s->cur.gn <= 0.5 * best_gn) {
         best_gn = s->cur.gn;
         since_best = 0;
-      } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr && s->cur.gn <= 100.0 * grad_tol) {
+      } else if (prm.stall_rtr > 0 && ++since_best > prm.stall_rtr && s->cur.gn <= prm.stall_factor * grad_tol) {
         // stagnation exit only near the tolerance (reading R30): far from it the inner solve
         // keeps going (an inexact subproblem solution steers the ALM multiplier update wrongly)
         last_exit = 1;

@@ -47,7 +47,7 @@ def test_default_params_match_design():
     # the library's defaults are the oracle's (readings R9-R16, R30)
     for k in ("sigma0", "sigma_min", "sigma_max", "gamma", "tau1", "tau2", "tol", "eig_neg_tol", "rank_tol",
               "eps_scale", "eps_floor", "p0", "max_outer", "max_rtr", "max_tcg", "escape_max", "rho_reg",
-              "stall_rtr", "precond_mu", "escape_gate"):
+              "stall_rtr", "precond_mu", "escape_gate", "stall_factor"):
         assert getattr(prm, k) == getattr(o, k), k
     assert prm.mode == 0 and o.mode == "alm"
 
