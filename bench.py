@@ -496,6 +496,8 @@ def run_gpu(args):
                            "not_converged", "outer_iters": info["outer_iters"], "p_max": info["p_max"],
                            "eta_p": info["eta_p"], "eta_d": info["eta_d"], "eta_g": info["eta_g"],
                            "dual_obj": info["dual_obj"], "n_costgrad": info["n_costgrad"], "n_hvp": info["n_hvp"]})
+            print(f"[bench] solve d={d} seed={seed}: {wall:.2f} s {solves[-1]['status']} outer={info['outer_iters']}",
+                  file=sys.stderr, flush=True)
         out["solves"] = solves
         # clique-chain sparse BQPs (multi-block relaxation), N(0,1) data as
         # in the paper; the paper's ManiDSDP means (Tables 2-3) as context
@@ -520,6 +522,8 @@ def run_gpu(args):
                           "outer_iters": info["outer_iters"], "p_max": info["p_max"], "eta_p": info["eta_p"],
                           "eta_d": info["eta_d"], "eta_g": info["eta_g"], "dual_obj": info["dual_obj"],
                           "n_costgrad": info["n_costgrad"], "n_hvp": info["n_hvp"]})
+            print(f"[bench] chain q={q} t={t}: {wall:.2f} s {chain[-1]['status']} outer={info['outer_iters']} "
+                  f"eta=({info['eta_p']:.1e},{info['eta_d']:.1e},{info['eta_g']:.1e})", file=sys.stderr, flush=True)
         out["chain_solves"] = chain
 
     # ---------------- cpu baseline (oracle, bounded sample) ------------------------------------

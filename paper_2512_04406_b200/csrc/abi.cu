@@ -565,9 +565,10 @@ int blk_dual(drsdp_ctx *ctx, int p, const double *Y, int ldv, const double *y, d
 
 static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y,
                                int ldv, double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost,
-                               double *egrad, double *rgrad);
+                               double *egrad, double *rgrad, double *Dbuf);
 static int alm_hvp_blocks(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv,
-                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp);
+                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp,
+                          double *Zbuf);
 
 // y-eliminated subproblem at Y: y(S), M(S) (materialised into Mout), cost/gradients.
 static bool use_dense(const double *Y, const double *U, int ldv) {
@@ -579,7 +580,8 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
                  double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost, double *egrad,
                  double *rgrad, double *Dbuf) {
   Problem &P = ctx->prob;
-  if (P.nblk > 0) return alm_costgrad_blocks(ctx, p, T, ldt, sigma, Y, ldv, Mout, ldm, yS, G, rho, cost, egrad, rgrad);
+  if (P.nblk > 0)
+    return alm_costgrad_blocks(ctx, p, T, ldt, sigma, Y, ldv, Mout, ldm, yS, G, rho, cost, egrad, rgrad, Dbuf);
   const int n = (int)P.n;
   int rc = ensure_workspace(ctx, n, p);
   if (rc) return rc;
@@ -637,7 +639,7 @@ int alm_costgrad(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sig
 int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv, const double *U,
             const double *G, double *K, const double *rho, double *wZ, double *hvp, double *Zbuf) {
   Problem &P = ctx->prob;
-  if (P.nblk > 0) return alm_hvp_blocks(ctx, p, M, ldm, Y, ldv, U, G, K, rho, wZ, hvp);
+  if (P.nblk > 0) return alm_hvp_blocks(ctx, p, M, ldm, Y, ldv, U, G, K, rho, wZ, hvp, Zbuf);
   const int n = (int)P.n;
   // K = U^T Y + Y^T U runs on the auxiliary stream, concurrently with Z and its segmented sum
   // (fork / join with events; inside a graph capture this becomes two parallel branches)
@@ -696,7 +698,7 @@ int alm_hvp(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y
 // with the S tiles, then the block product with the COSTGRAD row epilogue.
 static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, double sigma, const double *Y,
                                int ldv, double *Mout, int64_t ldm, double *yS, double *G, double *rho, double *cost,
-                               double *egrad, double *rgrad) {
+                               double *egrad, double *rgrad, double *Dbuf) {
   Problem &P = ctx->prob;
   const int t = (int)P.nblk, nb = (int)P.nb;
   if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
@@ -704,8 +706,18 @@ static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t l
   if (rc) return rc;
   KL(blk_gram_launch(t, nb, p, Y, ldv, nullptr, 0, G, nullptr, ctx->skip_flag, ctx->stream), "block gram");
   SegArgs s = seg_args(ctx, p, Y, nullptr, ldv, yS);
+  if (Dbuf) {
+    // S_k = Y_k Y_k^T as dense stacked tiles: the segmented sum gathers one entry per position and
+    // the assembly reads them back (instead of p-length dot products per position)
+    KL(blk_tile_launch(t, nb, p, Y, nullptr, ldv, Dbuf, P.ld, ctx->skip_flag, ctx->stream), "block tiles (S)");
+    s.D = Dbuf;
+    s.ldd = P.ld;
+    s.nbk = nb;
+  }
   KL(segsum_launch(s, false, ctx->stream), "segsum kernel");
   BlkElemArgs e;
+  e.D = Dbuf;
+  e.ldd = P.ld;
   e.t = t;
   e.nb = nb;
   e.p = p;
@@ -746,12 +758,19 @@ static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t l
 // sum from Y, U rows), then one block product Q = M U + A*(w) Y (gather) with the HVP epilogue:
 // three launches per Hessian-vector product.
 static int alm_hvp_blocks(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, const double *Y, int ldv,
-                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp) {
+                          const double *U, const double *G, double *K, const double *rho, double *wZ, double *hvp,
+                          double *Zbuf) {
   Problem &P = ctx->prob;
   const int t = (int)P.nblk, nb = (int)P.nb;
   if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
   KL(blk_gram_launch(t, nb, p, Y, ldv, U, ldv, nullptr, K, ctx->skip_flag, ctx->stream), "block gram (K)");
   SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
+  if (Zbuf) {
+    KL(blk_tile_launch(t, nb, p, Y, U, ldv, Zbuf, P.ld, ctx->skip_flag, ctx->stream), "block tiles (Z)");
+    s.D = Zbuf;
+    s.ldd = P.ld;
+    s.nbk = nb;
+  }
   KL(segsum_launch(s, true, ctx->stream), "segsum kernel (Z)");
   SymvArgs a = base_symv(ctx, (int)P.n, p, M, ldm);
   a.V = U;
@@ -1607,7 +1626,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   CK(ctx->alm_K.ensure((size_t)p * p * gmul), "alloc K");
   int rc;
   if (flags & DRSDP_EVAL_COSTGRAD) {
-    if (!P.nblk) CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
+    CK(ctx->alm_D.ensure((size_t)n * P.ld), "alloc dense S");
     rc = alm_costgrad(ctx, p, T_dev, ldt, sigma, Y_dev, p, ctx->alm_M.ptr, P.ld, ctx->alm_yS.ptr, ctx->alm_G.ptr,
                       ctx->alm_rho.ptr, cost_dev, egrad_dev, rgrad_dev, ctx->alm_D.ptr);
     if (rc) return rc;
@@ -1621,7 +1640,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
     return set_error(ctx, DRSDP_ERR_STATE, "HVP needs a prior COSTGRAD at the same Y, T, sigma");
   }
   if (flags & DRSDP_EVAL_HVP) {
-    if (!P.nblk) CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
+    CK(ctx->alm_Z.ensure((size_t)n * P.ld), "alloc dense Z");
     rc = alm_hvp(ctx, p, ctx->alm_M.ptr, P.ld, Y_dev, p, U_dev, ctx->alm_G.ptr, ctx->alm_K.ptr, ctx->alm_rho.ptr,
                  ctx->alm_wZ.ptr, hvp_dev, ctx->alm_Z.ptr);
     if (rc) return rc;

@@ -107,7 +107,14 @@ __global__ void __launch_bounds__(256) blk_elem_kernel(BlkElemArgs a) {
   double s[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) s[q] = 0.0;
-  for (int c0 = 0; c0 < a.p; c0 += BE_PC) {
+  if (a.D) {  // S tiles already written by blk_tile (the segmented sum's input)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = i0 + ty + 4 * q, j = j0 + tx;
+      if (i < a.nb && j < a.nb) s[q] = a.D[(b0 + i) * a.ldd + j];
+    }
+  }
+  for (int c0 = 0; c0 < (a.D ? 0 : a.p); c0 += BE_PC) {
     const int pc = min(BE_PC, a.p - c0);
     __syncthreads();
     for (int t = threadIdx.x; t < BE_R * BE_PC; t += 256) {
@@ -150,6 +157,71 @@ __global__ void __launch_bounds__(256) blk_elem_kernel(BlkElemArgs a) {
     }
   }
   grid_sum<3>(v3, a.part, a.counter, a.scal_out, scratch);
+}
+
+// dense block tiles for the segmented sums (the block analogue of gram_tile.cu): D_k = Y_k Y_k^T
+// (full block: the assembly reads it back) or Z_k = Y_k U_k^T + U_k Y_k^T (upper tiles only: the
+// segmented sum reads upper positions), stacked rows, pitch ldd
+constexpr int BT_PC = 16;  // p chunk of the tile kernel (4 staged operands: 26 KB of static shared memory)
+
+template <bool ZM>
+__global__ void __launch_bounds__(256) blk_tile_kernel(int nb, int p, const double *__restrict__ Y,
+                                                       const double *__restrict__ U, int ldy, double *__restrict__ D,
+                                                       int64_t ldd, const int *skip) {
+  if (skip && *(volatile const int *)skip) return;
+  const int i0 = blockIdx.y * BE_R, j0 = blockIdx.x * BE_C;
+  if (ZM && j0 + BE_C <= i0) return;  // tile entirely below the diagonal
+  __shared__ double yr[BE_R][BT_PC + 1];
+  __shared__ double yc[BE_C][BT_PC + 1];
+  __shared__ double ur[ZM ? BE_R : 1][BT_PC + 1];
+  __shared__ double uc[ZM ? BE_C : 1][BT_PC + 1];
+  const int64_t b0 = (int64_t)blockIdx.z * nb;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  double s[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s[q] = 0.0;
+  for (int c0 = 0; c0 < p; c0 += BT_PC) {
+    const int pc = min(BT_PC, p - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < BE_R * BT_PC; t += 256) {
+      const int i = t / BT_PC, c = t - i * BT_PC;
+      const bool ok = i0 + i < nb && c < pc;
+      yr[i][c] = ok ? Y[(b0 + i0 + i) * ldy + c0 + c] : 0.0;
+      if (ZM) ur[i][c] = ok ? U[(b0 + i0 + i) * ldy + c0 + c] : 0.0;
+    }
+    for (int t = threadIdx.x; t < BE_C * BT_PC; t += 256) {
+      const int j = t / BT_PC, c = t - j * BT_PC;
+      const bool ok = j0 + j < nb && c < pc;
+      yc[j][c] = ok ? Y[(b0 + j0 + j) * ldy + c0 + c] : 0.0;
+      if (ZM) uc[j][c] = ok ? U[(b0 + j0 + j) * ldy + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < pc; ++c) {
+      const double v = yc[tx][c];
+      const double w = ZM ? uc[tx][c] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        s[q] = fma(yr[ty + 4 * q][c], ZM ? w : v, s[q]);
+        if (ZM) s[q] = fma(ur[ty + 4 * q][c], v, s[q]);
+      }
+    }
+  }
+  const int j = j0 + tx;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i = i0 + ty + 4 * q;
+    if (i < nb && j < nb) D[(b0 + i) * ldd + j] = s[q];
+  }
+}
+
+cudaError_t blk_tile_launch(int t, int nb, int p, const double *Y, const double *U, int ldy, double *D, int64_t ldd,
+                            const int *skip, cudaStream_t st) {
+  dim3 grid((nb + BE_C - 1) / BE_C, (nb + BE_R - 1) / BE_R, t);
+  if (U)
+    blk_tile_kernel<true><<<grid, 256, 0, st>>>(nb, p, Y, U, ldy, D, ldd, skip);
+  else
+    blk_tile_kernel<false><<<grid, 256, 0, st>>>(nb, p, Y, nullptr, ldy, D, ldd, skip);
+  return cudaGetLastError();
 }
 
 int blk_elem_blocks(int t, int nb) { return t * ((nb + BE_R - 1) / BE_R) * ((nb + BE_C - 1) / BE_C); }

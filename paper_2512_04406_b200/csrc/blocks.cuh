@@ -32,6 +32,8 @@ struct BlkElemArgs {
   double sigma = 1.0;
   double *M = nullptr;  // ASM output M = A*(y) - T/sigma
   int64_t ldmo = 0;
+  const double *D = nullptr;  // ASM: S tiles from blk_tile (stacked, pitch ldd) instead of recomputing
+  int64_t ldd = 0;
   double *part = nullptr;
   unsigned *counter = nullptr;
   // ASM: [sum (S - A*(y))^2, <T, S>, ||T||^2] (the accurate ALM cost, reading R29)
@@ -41,6 +43,10 @@ struct BlkElemArgs {
 // S_k tiles recomputed from Y (32 x 64 tiles, p in chunks of 32) fused with the elementwise work
 cudaError_t blk_elem_launch(const BlkElemArgs &a, int mode, cudaStream_t st);
 int blk_elem_blocks(int t, int nb);
+
+// D_k = Y_k Y_k^T (U == nullptr, full blocks) or Y_k U_k^T + U_k Y_k^T (upper tiles), stacked
+cudaError_t blk_tile_launch(int t, int nb, int p, const double *Y, const double *U, int ldy, double *D, int64_t ldd,
+                            const int *skip, cudaStream_t st);
 
 // T = A*(b / cnt) on every block (T^0 = D, X~^0 = 0)
 cudaError_t blk_initd_launch(int t, int nb, const int32_t *amap, int64_t ldm, const double *b, const int32_t *cnt,

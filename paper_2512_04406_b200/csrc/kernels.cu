@@ -161,10 +161,11 @@ cudaError_t gram_launch(const GramArgs &a, cudaStream_t st) {
 // ----------------------------------------------------------------------------------------------
 template <bool ZMODE>
 DRSDP_DEV double seg_pos_value(uint32_t pk, const double *__restrict__ Y, const double *__restrict__ U, int ld,
-                               int p, const double *__restrict__ D, int64_t ldd) {
+                               int p, const double *__restrict__ D, int64_t ldd, int nbk) {
   const int i = pk >> 16, j = pk & 0xffff;
   if (D) {
-    const double v = __ldg(D + (size_t)i * ldd + j);
+    // block problems: D is stacked (row i holds the columns of its own block of nbk rows)
+    const double v = __ldg(D + (size_t)i * ldd + (nbk ? j - i / nbk * nbk : j));
     return (i == j) ? v : 2.0 * v;
   }
   const double *yi = Y + (size_t)i * ld, *yj = Y + (size_t)j * ld;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     if (s < a.m && !a.is_large[s]) {
       const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
       double acc = 0.0;
-      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
+      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk);
       if (!ZMODE && a.cA) acc += a.cA[s];
       a.out[s] = acc / (double)a.cnt[s];
       if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
       const int s = a.large_ids[li];
       const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
       double acc = 0.0;
-      for (int64_t k = b0 + lane; k < b1; k += 32) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
+      for (int64_t k = b0 + lane; k < b1; k += 32) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (!ZMODE && a.cA) acc += a.cA[s];
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
     double acc[1] = {0.0};
     for (int64_t k = b0 + threadIdx.x; k < b1; k += blockDim.x)
-      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd);
+      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk);
     block_sum<1>(acc, scratch);
     if (threadIdx.x == 0) {
       double t = acc[0];

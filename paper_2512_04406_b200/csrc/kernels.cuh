@@ -42,6 +42,7 @@ struct SegArgs {
   // of the p-length dot products; D = Y Y^T (MODE_Y) or Y U^T + U Y^T (MODE_Z)
   const double *D = nullptr;
   int64_t ldd = 0;
+  int nbk = 0;  // block problems: D stacked with blocks of nbk rows (blocks.cuh)
 };
 cudaError_t segsum_launch(const SegArgs &a, bool zmode, cudaStream_t st);
 int segsum_blocks(int64_t m, int64_t n_large, int64_t n_huge);

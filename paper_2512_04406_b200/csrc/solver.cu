@@ -512,9 +512,9 @@ static int alloc_solver(drsdp_ctx *ctx, int p0) {
     CK(s->Mbuf[k].ensure((size_t)P.n * P.ld), "alloc M");
     CK(s->rhobuf[k].ensure(P.n), "alloc");
     CK(s->ySbuf[k].ensure(P.m), "alloc");
-    if (std::getenv("DRSDP_NO_DENSE") == nullptr && !P.nblk) CK(s->Dbuf[k].ensure((size_t)P.n * P.ld), "alloc dense S");
+    if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Dbuf[k].ensure((size_t)P.n * P.ld), "alloc dense S");
   }
-  if (std::getenv("DRSDP_NO_DENSE") == nullptr && !P.nblk) CK(s->Zbuf.ensure((size_t)P.n * P.ld), "alloc dense Z");
+  if (std::getenv("DRSDP_NO_DENSE") == nullptr) CK(s->Zbuf.ensure((size_t)P.n * P.ld), "alloc dense Z");
   s->ldp = 0;
   RC(set_pitch(ctx, std::max(64, ((p0 + 63) / 64) * 64), false, 0));
   CK(s->wZ.ensure(P.m), "alloc");
