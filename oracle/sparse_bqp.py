@@ -234,24 +234,28 @@ def block_residues(amaps, cnt, b, y, Y, T):
 
 
 def block_escape_directions(lams, Vs, eig_neg_tol, escape_max):
-    """Escape directions of the block-diagonal X (Thm 4.5; reading R39): the eigenpairs of
-    all blocks with lambda < -eig_neg_tol (1 + |lambda_max|), most negative first (ties: lower
-    block first), at most escape_max, each embedded in its block's rows (zeros elsewhere); sign
-    so that the largest-|.| entry is positive (R25). Returns an N x delta array or None."""
+    """Escape directions of the block-diagonal X (Thm 4.5, on the product of the blocks'
+    manifolds; reading R39): in every block, the eigenpairs with lambda < -eig_neg_tol (1 + |lambda_max|)
+    (lambda_max over all blocks), most negative first; column c of the result holds the c-th such
+    eigenvector of EVERY block that has one, in that block's rows (zeros elsewhere) — the blocks do not
+    interact, so one new column escapes in all blocks at once. delta = min(escape_max, max_k #neg_k)
+    columns; each block's vector signed so that its largest-|.| entry is positive (R25). Returns an
+    N x delta array or None. For t = 1 this is oracle/admm.escape_directions."""
     t, nb = len(lams), lams[0].size
     lam_max = max(float(l[-1]) for l in lams)
     thresh = -eig_neg_tol * (1.0 + abs(lam_max))
-    cand = sorted((float(lams[k][i]), k, i) for k in range(t) for i in range(nb) if lams[k][i] < thresh)
-    cand = cand[:escape_max]
-    if not cand:
+    negs = [int(np.sum(l < thresh)) for l in lams]  # eigh: ascending
+    delta = min(escape_max, max(negs))
+    if delta == 0:
         return None
-    out = np.zeros((t * nb, len(cand)))
-    for c, (_, k, i) in enumerate(cand):
-        v = Vs[k][:, i].copy()
-        j = int(np.argmax(np.abs(v)))
-        if v[j] < 0:
-            v = -v
-        out[k * nb:(k + 1) * nb, c] = v
+    out = np.zeros((t * nb, delta))
+    for k in range(t):
+        for c in range(min(delta, negs[k])):
+            v = Vs[k][:, c].copy()
+            j = int(np.argmax(np.abs(v)))
+            if v[j] < 0:
+                v = -v
+            out[k * nb:(k + 1) * nb, c] = v
     return out
 
 
@@ -310,8 +314,9 @@ def solve_blocks(amaps, cnt, b, prm: Params, Y0: np.ndarray, verbose=False):
             trace.append(row)
             break
         Vs = block_escape_directions(res["lams"], res["Vs"], prm.eig_neg_tol, prm.escape_max)
-        if Vs is not None and Y.shape[1] + Vs.shape[1] > N:
-            Vs = Vs[:, : N - Y.shape[1]] if Y.shape[1] < N else None
+        pcap = min(64, nb)  # reading R39: p <= min(64, n_b) for block problems
+        if Vs is not None and Y.shape[1] + Vs.shape[1] > pcap:
+            Vs = Vs[:, : pcap - Y.shape[1]] if Y.shape[1] < pcap else None
         gated = prm.escape_gate > 0 and info["gnorm"] > prm.escape_gate * grad_tol
         if gated:
             Vs = None

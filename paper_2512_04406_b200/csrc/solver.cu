@@ -792,7 +792,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     // block problems: the spectrum of the block-diagonal X is the union of the blocks' spectra
     // (reading R38); all blocks in one batched decomposition, merged on the host in ascending
     // order (ties: lower block, then lower index first), escape vectors embedded in their rows
-    std::vector<std::pair<int, int>> blk_src;  // (block, eigen index) of lam[i]
+    std::vector<double> blk_w;  // per-block ascending eigenvalues (block k at k * n_b)
     auto block_eig = [&]() -> int {
       KL(blk_makex_launch(nblk, nbk, s->T.ptr, P.ld, s->z.ptr, s->X.ptr, ctx->stream), "make X (blocks)");
       if (cusolverDnXsyevBatched(s->sol, s->sparams, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, nbk, CUDA_R_64F,
@@ -801,7 +801,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
                                  nblk) != CUSOLVER_STATUS_SUCCESS)
         return set_error(ctx, DRSDP_ERR_CUDA, "cusolverDnXsyevBatched");
       ctx->launches++;
-      std::vector<double> wb((size_t)n);
+      std::vector<double> &wb = blk_w;
+      wb.resize((size_t)n);
       std::vector<int> infos(nblk);
       CK(cudaMemcpyAsync(wb.data(), s->W.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream), "read eig");
       CK(cudaMemcpyAsync(infos.data(), s->binfo.ptr, sizeof(int) * nblk, cudaMemcpyDeviceToHost, ctx->stream),
@@ -810,15 +811,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       for (int k2 = 0; k2 < nblk; ++k2)
         if (infos[k2] != 0)
           return set_error(ctx, DRSDP_ERR_NUMERIC, "batched eigen-decomposition failed (block " + std::to_string(k2) + ")");
-      std::vector<std::pair<double, std::pair<int, int>>> all((size_t)n);
-      for (int k2 = 0; k2 < nblk; ++k2)
-        for (int i = 0; i < nbk; ++i) all[(size_t)k2 * nbk + i] = {wb[(size_t)k2 * nbk + i], {k2, i}};
-      std::sort(all.begin(), all.end());
-      blk_src.resize(n);
-      for (int i = 0; i < n; ++i) {
-        lam[i] = all[i].first;
-        blk_src[i] = all[i].second;
-      }
+      for (int i = 0; i < n; ++i) lam[i] = wb[i];
+      std::sort(lam.begin(), lam.end());
       nlam = n;
       lam_top = lam[n - 1];
       vec_cols = nullptr;
@@ -875,7 +869,16 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     // escape directions: eigenvectors (Ritz vectors) with lambda < -eig_neg_tol (1 + |lambda_max|)
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam_top));
     int dv = 0;
-    while (dv < prm.escape_max && dv < nlam && dv < (dense_done ? n : nvec) && lam[dv] < thresh) ++dv;
+    std::vector<int> blk_neg;  // block problems: negative eigenvalues per block (reading R39)
+    if (blocks) {
+      blk_neg.assign(nblk, 0);
+      for (int k2 = 0; k2 < nblk; ++k2) {
+        while (blk_neg[k2] < nbk && blk_w[(size_t)k2 * nbk + blk_neg[k2]] < thresh) ++blk_neg[k2];
+        dv = std::max(dv, std::min(prm.escape_max, blk_neg[k2]));
+      }
+    } else {
+      while (dv < prm.escape_max && dv < nlam && dv < (dense_done ? n : nvec) && lam[dv] < thresh) ++dv;
+    }
     if (dv > 0 && p + dv > pcap) dv = std::max(0, pcap - p);
     // escape gate (reading R36): the certificate X^{k+1} is the subproblem's (Prop 4.3) only at a
     // stationary point; while the inner solve ends far above its tolerance, keep the rank (no escape,
@@ -929,19 +932,29 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       // canonical signs (largest-|.| entry positive), then Y <- [Y, 0], U <- [0, V]
       std::vector<double> Vh((size_t)n * dv, 0.0);
       if (blocks) {
-        // eigenvector i of block k (column i of the column-major X_k) into rows k n_b .. of column c
-        for (int c = 0; c < dv; ++c) {
-          const int kb = blk_src[c].first, ib = blk_src[c].second;
-          CK(cudaMemcpyAsync(Vh.data() + (size_t)c * n + (size_t)kb * nbk, s->X.ptr + ((size_t)kb * nbk + ib) * nbk,
-                             sizeof(double) * nbk, cudaMemcpyDeviceToHost, ctx->stream),
-             "read V");
-        }
+        // reading R39: column c holds the c-th most negative eigenvector of every block that has one
+        // (its rows only); the first dv eigenvectors of each block are contiguous in the column-major
+        // X_k, so one strided copy brings them all
+        std::vector<double> Vb((size_t)nblk * dv * nbk);
+        CK(cudaMemcpy2DAsync(Vb.data(), sizeof(double) * dv * nbk, s->X.ptr, sizeof(double) * nbk * nbk,
+                             sizeof(double) * dv * nbk, nblk, cudaMemcpyDeviceToHost, ctx->stream),
+           "read V");
+        CK(cudaStreamSynchronize(ctx->stream), "sync");
+        for (int k2 = 0; k2 < nblk; ++k2)
+          for (int c = 0; c < std::min(dv, blk_neg[k2]); ++c) {
+            const double *v = &Vb[((size_t)k2 * dv + c) * nbk];
+            int km = 0;
+            for (int i = 1; i < nbk; ++i)
+              if (std::fabs(v[i]) > std::fabs(v[km])) km = i;
+            const double sg = v[km] < 0 ? -1.0 : 1.0;  // canonical sign per block (reading R25)
+            for (int i = 0; i < nbk; ++i) Vh[(size_t)c * n + (size_t)k2 * nbk + i] = sg * v[i];
+          }
       } else {
         CK(cudaMemcpyAsync(Vh.data(), vec_cols, sizeof(double) * n * dv, cudaMemcpyDeviceToHost, ctx->stream),
            "read V");
       }
       CK(cudaStreamSynchronize(ctx->stream), "sync");
-      for (int c = 0; c < dv; ++c) {
+      for (int c = 0; c < (blocks ? 0 : dv); ++c) {
         int km = 0;
         for (int i = 1; i < n; ++i)
           if (std::fabs(Vh[(size_t)c * n + i]) > std::fabs(Vh[(size_t)c * n + km])) km = i;

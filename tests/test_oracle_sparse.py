@@ -149,24 +149,40 @@ def test_block_alm_is_the_y_eliminated_lagrangian():
     assert abs(0.5 * sigma * f - np.sum(T * T) / (2 * sigma) - Lmin) <= 1e-9 * (1 + abs(Lmin))
 
 
-def test_block_escape_directions_match_dense_eigh():
-    """The union of the per-block spectra is the spectrum of the block-diagonal X: the escape
-    directions equal the dense eigh escape directions of the assembled N x N matrix."""
+def test_block_escape_directions():
+    """t = 1: the dense escape rule (oracle/admm.escape_directions). t > 1: column c carries the
+    c-th most negative eigenvector of every block with one (reading R39), each a unit eigenvector
+    of its block with negative curvature, so <[0,V], 4 X [0,V]> < 0 (Thm 4.5)."""
     rng = np.random.default_rng(8)
-    t, nb = 3, 6
-    blocks = []
-    for k in range(t):
-        A = rng.standard_normal((nb, nb))
-        blocks.append((A + A.T) / 2)
-    lams, Vs = zip(*[np.linalg.eigh(B) for B in blocks])
-    Xd = np.zeros((t * nb, t * nb))
-    for k in range(t):
-        Xd[k * nb:(k + 1) * nb, k * nb:(k + 1) * nb] = blocks[k]
-    lam, V = np.linalg.eigh(Xd)
+    nb = 6
+    A = rng.standard_normal((nb, nb))
+    B = (A + A.T) / 2
+    lam, V = np.linalg.eigh(B)
     for emax in (1, 3, 5):
-        Eb = sb.block_escape_directions(list(lams), list(Vs), 1e-9, emax)
-        Ed = admm.escape_directions(lam, V, 1e-9, emax)
-        np.testing.assert_allclose(Eb, Ed, atol=1e-10)
+        np.testing.assert_allclose(sb.block_escape_directions([lam], [V], 1e-9, emax),
+                                   admm.escape_directions(lam, V, 1e-9, emax), atol=1e-12)
+    blocks = []
+    for k in range(3):
+        A = rng.standard_normal((nb, nb))
+        blocks.append((A + A.T) / 2 + (k - 1) * 1.5 * np.eye(nb))  # different numbers of negative eigenvalues
+    lams, Vs = zip(*[np.linalg.eigh(Bk) for Bk in blocks])
+    negs = [int(np.sum(l < -1e-9 * (1 + max(float(x[-1]) for x in lams)))) for l in lams]
+    E = sb.block_escape_directions(list(lams), list(Vs), 1e-9, 4)
+    assert E.shape[1] == min(4, max(negs))
+    for k in range(3):
+        Ek = E[k * nb:(k + 1) * nb]
+        for c in range(E.shape[1]):
+            v = Ek[:, c]
+            if c < negs[k]:
+                assert abs(np.linalg.norm(v) - 1) < 1e-12
+                np.testing.assert_allclose(blocks[k] @ v, lams[k][c] * v, atol=1e-10)
+                assert v[np.argmax(np.abs(v))] > 0
+            else:
+                assert not v.any()
+    Xd = np.zeros((3 * nb, 3 * nb))
+    for k in range(3):
+        Xd[k * nb:(k + 1) * nb, k * nb:(k + 1) * nb] = blocks[k]
+    assert np.trace(E.T @ Xd @ E) < 0
 
 
 def _chain_solve(q, t, seed, p0=2):

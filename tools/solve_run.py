@@ -1,6 +1,7 @@
 """Development aid: run drsdp_solve on BQP configs and print the per-iteration trace.
 
 Usage: python tools/solve_run.py D[,D...] [time_limit_s] [p0] [key=value ...]  (extra drsdp_params)
+       D may be chain:q:t (the clique-chain sparse BQP, multi-block relaxation)
 """
 import json
 import sys
@@ -11,16 +12,22 @@ from inputs import bqp_instance, initial_factor  # noqa: E402
 from oracle import bqp  # noqa: E402  (sizes only: n for the initial factor)
 from paper_2512_04406_b200 import abi  # noqa: E402
 
-ds = [int(x) for x in sys.argv[1].split(",")]
+ds = [x if x.startswith("chain") else int(x) for x in sys.argv[1].split(",")]
 tl = float(sys.argv[2]) if len(sys.argv) > 2 else 300.0
 ctx = abi.Context(0, None)
 for d in ds:
-    kind = "er05" if d == 150 else "dense"
-    Q, c = bqp_instance(d, 0, kind)
     t0 = time.time()
-    ctx.set_bqp(Q, c)
+    if isinstance(d, str):
+        from inputs import chain_bqp_instance  # noqa: E402
+
+        _, q, t = d.split(":")
+        ctx.set_bqp_chain(*chain_bqp_instance(int(q), int(t), 0))
+    else:
+        kind = "er05" if d == 150 else "dense"
+        Q, c = bqp_instance(d, 0, kind)
+        ctx.set_bqp(Q, c)
     n = ctx.sizes()[0]
-    p0 = int(sys.argv[3]) if len(sys.argv) > 3 else (2 if d <= 10 else 4)
+    p0 = int(sys.argv[3]) if len(sys.argv) > 3 else (2 if isinstance(d, str) or d <= 10 else 4)
     kw = {}
     for a in sys.argv[4:]:
         k, v = a.split("=")
