@@ -189,7 +189,20 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     if (s < a.m && !a.is_large[s]) {
       const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
       double acc = 0.0;
-      for (int64_t k = b0; k < b1; ++k) acc += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk);
+      // up to 8 positions per step with all their loads in flight (a serial walk paid two dependent
+      // L2/HBM round trips per position); the sum keeps the position order, so results are unchanged
+      for (int64_t k = b0; k < b1; k += 8) {
+        const int cn = (int)min((int64_t)8, b1 - k);
+        uint32_t pk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pk[u] = u < cn ? __ldg(a.seg_pos + k + u) : 0u;
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = u < cn ? seg_pos_value<ZMODE>(pk[u], a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u < cn) acc += v[u];
+      }
       if (!ZMODE && a.cA) acc += a.cA[s];
       a.out[s] = acc / (double)a.cnt[s];
       if (!ZMODE) sq = acc * acc / (double)a.cnt[s];
