@@ -98,7 +98,7 @@ int drsdp_set_bqp(drsdp_ctx *ctx, int32_t d, const double *Q, const double *c);
  * rows k*nb .. (k+1)*nb - 1); only the diagonal blocks exist. Uniform block size nb.
  * Solver differences (readings R37-R39): no tCG preconditioner; the eigen step is one
  * batched decomposition of all blocks (cusolverDnXsyevBatched), eta_d and the escape directions
- * from the union of the blocks' spectra; p <= min(64, nb); ALM mode only.
+ * from the union of the blocks' spectra; p <= min(128, nb); ALM mode only.
  * Every call below (solve, alm_eval, y_update, dual_update, get_solution, export_index_map)
  * accepts a block problem with these layouts:
  *   T, M (device): n x ldt "stacked" — row r holds the nb columns of its block (ldt >= nb);

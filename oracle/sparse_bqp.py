@@ -314,7 +314,7 @@ def solve_blocks(amaps, cnt, b, prm: Params, Y0: np.ndarray, verbose=False):
             trace.append(row)
             break
         Vs = block_escape_directions(res["lams"], res["Vs"], prm.eig_neg_tol, prm.escape_max)
-        pcap = min(64, nb)  # reading R39: p <= min(64, n_b) for block problems
+        pcap = min(128, nb)  # reading R39: p <= min(128, n_b) for block problems
         if Vs is not None and Y.shape[1] + Vs.shape[1] > pcap:
             Vs = Vs[:, : pcap - Y.shape[1]] if Y.shape[1] < pcap else None
         gated = prm.escape_gate > 0 and info["gnorm"] > prm.escape_gate * grad_tol

@@ -526,7 +526,7 @@ static int blk_tiles(drsdp_ctx *ctx, SymvArgs &a) {
 
 int blk_rowdot(drsdp_ctx *ctx, int p, const double *T, int64_t ldt, const double *Y, int ldv, double *z, double *zsum) {
   const Problem &P = ctx->prob;
-  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 128");
   SymvArgs a = base_symv(ctx, (int)P.n, p, T, ldt);
   a.V = Y;
   a.ldv = ldv;
@@ -701,7 +701,7 @@ static int alm_costgrad_blocks(drsdp_ctx *ctx, int p, const double *T, int64_t l
                                double *egrad, double *rgrad, double *Dbuf) {
   Problem &P = ctx->prob;
   const int t = (int)P.nblk, nb = (int)P.nb;
-  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 128");
   int rc = ensure_red(ctx, std::max<int64_t>(segsum_blocks(P.m, P.n_large, P.n_huge), blk_elem_blocks(t, nb)), 4);
   if (rc) return rc;
   KL(blk_gram_launch(t, nb, p, Y, ldv, nullptr, 0, G, nullptr, ctx->skip_flag, ctx->stream), "block gram");
@@ -762,7 +762,7 @@ static int alm_hvp_blocks(drsdp_ctx *ctx, int p, const double *M, int64_t ldm, c
                           double *Zbuf) {
   Problem &P = ctx->prob;
   const int t = (int)P.nblk, nb = (int)P.nb;
-  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 64");
+  if (p > kBlkMaxP) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems support p <= 128");
   KL(blk_gram_launch(t, nb, p, Y, ldv, U, ldv, nullptr, K, ctx->skip_flag, ctx->stream), "block gram (K)");
   SegArgs s = seg_args(ctx, p, Y, U, ldv, wZ);
   if (Zbuf) {
@@ -1617,7 +1617,7 @@ int drsdp_alm_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *T_dev
   const int n = (int)P.n;
   const size_t gmul = P.nblk > 0 ? (size_t)P.nblk : 1;  // one G, K per block
   if (P.nblk > 0 && (p > kBlkMaxP || ldt < P.nb))
-    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: block problems need p <= 64 and ldt >= nb");
+    return set_error(ctx, DRSDP_ERR_INVALID_ARG, "alm_eval: block problems need p <= 128 and ldt >= nb");
   CK(ctx->alm_M.ensure((size_t)n * P.ld), "alloc M");
   CK(ctx->alm_yS.ensure(P.m), "alloc yS");
   CK(ctx->alm_wZ.ensure(P.m), "alloc wZ");

@@ -15,7 +15,8 @@ namespace drsdp {
 // ------------------------------------------------------------------------------------------------
 // per-block Gram (P:239 per block): G_k = Y_k^T Y_k, K_k = U_k^T Y_k + Y_k^T U_k
 // ------------------------------------------------------------------------------------------------
-constexpr int BG_ROWS = 32;
+constexpr int BG_ROWS = 16;
+constexpr int BG_MAXO = 16;  // outputs per thread; a CTA covers 256 * 16 entries of G_k (grid.y chunks)
 
 __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const double *__restrict__ Y, int ldy,
                                                        const double *__restrict__ U, int ldu, double *__restrict__ G,
@@ -27,7 +28,8 @@ __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const doub
   const int k = blockIdx.x;
   const int64_t r0 = (int64_t)k * nb;
   const int pp = p * p;
-  constexpr int MAXO = kBlkMaxP * kBlkMaxP / 256;
+  const int o0 = blockIdx.y * 256 * BG_MAXO;
+  constexpr int MAXO = BG_MAXO;
   double g[MAXO], kk[MAXO];
 #pragma unroll
   for (int q = 0; q < MAXO; ++q) g[q] = kk[q] = 0.0;
@@ -42,7 +44,7 @@ __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const doub
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < MAXO; ++q) {
-      const int o = threadIdx.x + 256 * q;
+      const int o = o0 + threadIdx.x + 256 * q;
       if (o < pp) {
         const int a = o / p, b = o - a * p;
         double s = g[q], s2 = kk[q];
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const doub
   }
 #pragma unroll
   for (int q = 0; q < MAXO; ++q) {
-    const int o = threadIdx.x + 256 * q;
+    const int o = o0 + threadIdx.x + 256 * q;
     if (o < pp) {
       if (G) G[(size_t)k * pp + o] = g[q];
       if (K && U) K[(size_t)k * pp + o] = kk[q];
@@ -70,7 +72,8 @@ cudaError_t blk_gram_launch(int t, int nb, int p, const double *Y, int ldy, cons
                             double *K, const int *skip, cudaStream_t st) {
   if (p > kBlkMaxP) return cudaErrorInvalidValue;
   const size_t smem = sizeof(double) * BG_ROWS * p * (U ? 2 : 1);
-  blk_gram_kernel<<<t, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip);
+  const dim3 grid(t, (p * p + 256 * BG_MAXO - 1) / (256 * BG_MAXO));
+  blk_gram_kernel<<<grid, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip);
   return cudaGetLastError();
 }
 
@@ -281,7 +284,8 @@ template <int PT, int EPI, bool GATHER>
 __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, int nstrip) {
   if (a.skip && *(volatile const int *)a.skip) return;
   extern __shared__ double sm[];
-  constexpr bool NEEDG = EPI == EPI_COSTGRAD || EPI == EPI_HVP;
+  constexpr bool GSG = PT > 64;  // wide p: G_k, K_k read from global memory in the epilogue
+  constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && !GSG;
   const int p = a.p;
   double *gs = sm;                                        // 2 p^2 (G, K)
   double *ptile = gs + (NEEDG ? 2 * p * p : 0);           // BP_R x PT
@@ -337,19 +341,19 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
     if (o < BP_R * PT) ptile[o] = acc[q];
   }
   SymvArgs al = a;
-  if constexpr (NEEDG) {
+  if constexpr (EPI == EPI_COSTGRAD || EPI == EPI_HVP) {
     al.G = a.G + (size_t)k * p * p;
     if (a.K) al.K = a.K + (size_t)k * p * p;
   }
   __syncthreads();
-  tile_epilogue<PT, EPI, BP_R, 256>(al, ptile, gs, scratch, &s_ticket, tile, (int)r0, 0, (int)(b0 + nb), p);
+  tile_epilogue<PT, EPI, BP_R, 256, GSG>(al, ptile, gs, scratch, &s_ticket, tile, (int)r0, 0, (int)(b0 + nb), p);
 }
 
 int blk_product_tiles(int t, int nb) { return t * ((nb + BP_R - 1) / BP_R); }
 
 template <int PT, int EPI, bool GATHER>
 static cudaError_t launch_bp(const SymvArgs &a, int t, int nb, cudaStream_t st) {
-  constexpr bool NEEDG = EPI == EPI_COSTGRAD || EPI == EPI_HVP;
+  constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && PT <= 64;
   const int nstrip = (nb + BP_R - 1) / BP_R;
   const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * (BP_J + 1) + BP_J * PT +
                                         (GATHER ? BP_R * (BP_J + 1) + BP_J * PT : 0));
@@ -380,6 +384,7 @@ cudaError_t blk_product_launch(const SymvArgs &a, int epi, bool gather, int t, i
   if (a.p <= 16) return launch_bp_pt<16>(a, epi, gather, t, nb, st);
   if (a.p <= 32) return launch_bp_pt<32>(a, epi, gather, t, nb, st);
   if (a.p <= 64) return launch_bp_pt<64>(a, epi, gather, t, nb, st);
+  if (a.p <= 128) return launch_bp_pt<128>(a, epi, gather, t, nb, st);
   return cudaErrorInvalidValue;
 }
 

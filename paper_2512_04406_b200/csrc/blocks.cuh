@@ -11,7 +11,7 @@
 
 namespace drsdp {
 
-constexpr int kBlkMaxP = 64;  // factor width supported by the block kernels (p <= min(64, n_b))
+constexpr int kBlkMaxP = 128;  // factor width supported by the block kernels (p <= min(128, n_b))
 
 // G_k = Y_k^T Y_k and (U != nullptr) K_k = U_k^T Y_k + Y_k^T U_k, p x p each (pitch p), k < t
 cudaError_t blk_gram_launch(int t, int nb, int p, const double *Y, int ldy, const double *U, int ldu, double *G,

@@ -619,10 +619,10 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   int p = ctx->p0_given ? ctx->p0_given : prm.p0;
   const bool blocks = ctx->prob.nblk > 0;
   const int nblk = (int)ctx->prob.nblk, nbk = (int)ctx->prob.nb;
-  // rank cap: p <= n (S has rank <= n); block problems: p <= min(64, n_b) (blocks.cuh)
+  // rank cap: p <= n (S has rank <= n); block problems: p <= min(128, n_b) (blocks.cuh)
   const int pcap = blocks ? std::min(kBlkMaxP, nbk) : std::min<int>(DRSDP_MAX_P, (int)ctx->prob.n);
   if (blocks && prm.mode == 1) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems: ALM mode only");
-  if (blocks && p > pcap) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems: p0 <= min(64, n_b)");
+  if (blocks && p > pcap) return set_error(ctx, DRSDP_ERR_INVALID_ARG, "block problems: p0 <= min(128, n_b)");
   RC(alloc_solver(ctx, p));
   SolverState *s = ctx->solver;
   Problem &P = ctx->prob;

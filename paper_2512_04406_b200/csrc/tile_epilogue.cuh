@@ -11,17 +11,20 @@
 
 namespace drsdp {
 
-template <int PT, int EPI, int BMR, int NTH>
-DRSDP_DEV void tile_epilogue(const SymvArgs &a, const double *ptile, double *gs, double *scratch,
+// GS_GLOBAL: read G (and K) from global memory (L1/L2) instead of staging them in shared memory
+// (wide p, where 2 p^2 doubles exceed the shared-memory budget)
+template <int PT, int EPI, int BMR, int NTH, bool GS_GLOBAL = false>
+DRSDP_DEV void tile_epilogue(const SymvArgs &a, const double *ptile, double *gs_smem, double *scratch,
                              unsigned *s_ticket, int tile, int j0, int c0, int n, int p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NWARPS = NTH / 32;
   constexpr int CPL = (PT + 31) / 32;
-  if constexpr (EPI == EPI_COSTGRAD || EPI == EPI_HVP) {
-    for (int t = threadIdx.x; t < p * p; t += NTH) gs[t] = a.G[t];
+  if constexpr (!GS_GLOBAL && (EPI == EPI_COSTGRAD || EPI == EPI_HVP)) {
+    for (int t = threadIdx.x; t < p * p; t += NTH) gs_smem[t] = a.G[t];
     if constexpr (EPI == EPI_HVP)
-      for (int t = threadIdx.x; t < p * p; t += NTH) gs[p * p + t] = a.K[t];
+      for (int t = threadIdx.x; t < p * p; t += NTH) gs_smem[p * p + t] = a.K[t];
   }
+  const double *gs = GS_GLOBAL ? a.G : gs_smem;
   __syncthreads();
   double sc0 = 0.0, sc1 = 0.0;
   for (int jj = warp; jj < BMR; jj += NWARPS) {
@@ -96,7 +99,7 @@ DRSDP_DEV void tile_epilogue(const SymvArgs &a, const double *ptile, double *gs,
       double acc2[CPL];
 #pragma unroll
       for (int h = 0; h < CPL; ++h) acc2[h] = 0.0;
-      const double *ks = gs + p * p;
+      const double *ks = GS_GLOBAL ? a.K : gs + p * p;
       for (int k = 0; k < p; ++k) {
         const double yk = __shfl_sync(0xffffffffu, yv[k >> 5], k & 31);
         const double uk = __shfl_sync(0xffffffffu, uv[k >> 5], k & 31);

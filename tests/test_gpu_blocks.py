@@ -104,7 +104,7 @@ def _stacked(T, ld):
     return out
 
 
-@pytest.mark.parametrize("q,t,p", [(4, 3, 1), (5, 4, 3), (6, 3, 16), (8, 5, 17), (20, 3, 33), (20, 4, 64)])
+@pytest.mark.parametrize("q,t,p", [(4, 3, 1), (5, 4, 3), (6, 3, 16), (8, 5, 17), (20, 3, 33), (20, 4, 64), (20, 3, 100), (20, 2, 128)])
 def test_block_alm_eval_parity(ctx, q, t, p):
     from paper_2512_04406_b200 import abi
 
