@@ -6,6 +6,8 @@
 // per 16-32-row strip of a block, operands staged in shared memory, FP64 FMA (a 211-wide
 // contraction per output; DMMA fragments would not pay at these sizes). Reductions are fixed-order
 // (bit-reproducible). See blocks.cuh for the stacked layout.
+#include <algorithm>
+
 #include "blocks.cuh"
 #include "common.cuh"
 #include "tile_epilogue.cuh"
@@ -15,12 +17,14 @@ namespace drsdp {
 // ------------------------------------------------------------------------------------------------
 // per-block Gram (P:239 per block): G_k = Y_k^T Y_k, K_k = U_k^T Y_k + Y_k^T U_k
 // ------------------------------------------------------------------------------------------------
-constexpr int BG_ROWS = 16;
 constexpr int BG_MAXO = 16;  // outputs per thread; a CTA covers 256 * 16 entries of G_k (grid.y chunks)
+// rows of Y_k (and U_k) staged per step: as many as fit 64 KB (one step for p <= 16 at n_b = 211),
+// so that few dependent load rounds are paid per block
+inline int bg_rows(int nb, int p, bool u) { return std::max(16, std::min(nb, 8192 / (p * (u ? 2 : 1)))); }
 
 __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const double *__restrict__ Y, int ldy,
                                                        const double *__restrict__ U, int ldu, double *__restrict__ G,
-                                                       double *__restrict__ K, const int *skip) {
+                                                       double *__restrict__ K, const int *skip, int BG_ROWS) {
   if (skip && *(volatile const int *)skip) return;
   extern __shared__ double sm[];
   double *ys = sm;
@@ -71,9 +75,15 @@ __global__ void __launch_bounds__(256) blk_gram_kernel(int nb, int p, const doub
 cudaError_t blk_gram_launch(int t, int nb, int p, const double *Y, int ldy, const double *U, int ldu, double *G,
                             double *K, const int *skip, cudaStream_t st) {
   if (p > kBlkMaxP) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(double) * BG_ROWS * p * (U ? 2 : 1);
+  const int rows = bg_rows(nb, p, U != nullptr);
+  const size_t smem = sizeof(double) * rows * p * (U ? 2 : 1);
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(blk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   const dim3 grid(t, (p * p + 256 * BG_MAXO - 1) / (256 * BG_MAXO));
-  blk_gram_kernel<<<grid, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip);
+  blk_gram_kernel<<<grid, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip, rows);
   return cudaGetLastError();
 }
 

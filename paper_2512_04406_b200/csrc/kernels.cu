@@ -227,8 +227,21 @@ __global__ void __launch_bounds__(256) segsum_kernel(SegArgs a) {
     const int s = a.huge_ids[blockIdx.x - a.nb_small - a.nb_large];
     const int64_t b0 = a.seg_ptr[s], b1 = a.seg_ptr[s + 1];
     double acc[1] = {0.0};
-    for (int64_t k = b0 + threadIdx.x; k < b1; k += blockDim.x)
-      acc[0] += seg_pos_value<ZMODE>(__ldg(a.seg_pos + k), a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk);
+    // 8 strided positions per thread and step with their loads in flight (multi-block problems put
+    // ~10^2 diagonal positions on every thread); per-thread order unchanged
+    const int64_t bs = blockDim.x;
+    for (int64_t k0 = b0 + threadIdx.x; k0 < b1; k0 += 8 * bs) {
+      uint32_t pk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pk[u] = k0 + u * bs < b1 ? __ldg(a.seg_pos + k0 + u * bs) : 0u;
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = k0 + u * bs < b1 ? seg_pos_value<ZMODE>(pk[u], a.Y, a.U, a.ld, a.p, a.D, a.ldd, a.nbk) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u * bs < b1) acc[0] += v[u];
+    }
     block_sum<1>(acc, scratch);
     if (threadIdx.x == 0) {
       double t = acc[0];
