@@ -250,7 +250,10 @@ enum { DRSDP_EVAL_COSTGRAD = 1, DRSDP_EVAL_HVP = 2 };
  * Riemannian Hessian. flags: COSTGRAD computes cost/egrad/rgrad (any output pointer may be NULL);
  * HVP computes hvp and needs U_dev; HVP without COSTGRAD in the same call reuses the Gram matrix
  * and rowdot(E, Y) cached by the last COSTGRAD call at the same Y_dev and p (else ERR_STATE).
- * 1 <= p <= DRSDP_MAX_P. */
+ * COSTGRAD | HVP in one call with 5 <= p <= 32 runs ONE pass over M: the product M [Y U] (2p
+ * columns, TMA + DMMA) with the cost/gradient epilogue on the Y half and the Hessian-vector
+ * epilogue on the U half of each row (same arithmetic as two separate calls; M is streamed once
+ * instead of twice). 1 <= p <= DRSDP_MAX_P. */
 int drsdp_subproblem_eval(drsdp_ctx *ctx, int32_t flags, int32_t p, const double *Y_dev,
                           const double *U_dev, double *cost_dev, double *egrad_dev,
                           double *rgrad_dev, double *hvp_dev);
@@ -308,7 +311,8 @@ int drsdp_launch_count(drsdp_ctx *ctx, int64_t *count);
 int drsdp_profile_enable(drsdp_ctx *ctx, int enable);
 
 /* Total device milliseconds and launch count of the product kernel since profile_enable, for
- * kind 0 = all launches, 1 = COSTGRAD epilogue, 2 = HVP epilogue, 3 = other (RAW/ROWDOT).
+ * kind 0 = all launches, 1 = COSTGRAD epilogue, 2 = HVP epilogue, 3 = other (RAW/ROWDOT),
+ * 4 = fused COSTGRAD + HVP (one pass over M, drsdp_subproblem_eval with both flags, 5 <= p <= 32).
  * Synchronizes the context stream. */
 int drsdp_profile_read(drsdp_ctx *ctx, int32_t kind, double *ms, int64_t *launches);
 

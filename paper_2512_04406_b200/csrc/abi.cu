@@ -157,9 +157,9 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     a.rows_per_split = ((ktot + S - 1) / S + bk - 1) / bk * bk;
     if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bm * pt), "alloc split workspace");
     CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
-    CK(ctx->tile_scal.ensure((size_t)ntiles * 2), "alloc tile scalars");
+    CK(ctx->tile_scal.ensure((size_t)ntiles * 3), "alloc tile scalars");
     const int64_t ldvt = (kn + 1) / 2 * 2;
-    CK(ctx->vt_buf.ensure((size_t)(pair ? 2 : 1) * a.p * ldvt), "alloc V^T");
+    CK(ctx->vt_buf.ensure((size_t)(pair || epi == EPI_BOTH ? 2 : 1) * a.p * ldvt), "alloc V^T");
     if (!pair) a.A2 = nullptr;
     a.part = ctx->symv_part.ptr;
     a.tile_cnt = ctx->tile_cnt.ptr;
@@ -167,7 +167,7 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     a.glob_cnt = ctx->counters + C_SYMV;
     int rc = prof_kind ? prof_begin(ctx, prof_kind) : DRSDP_OK;
     if (rc) return rc;
-    ctx->launches++;  // transpose
+    ctx->launches += epi == EPI_BOTH ? 2 : 1;  // transposes
     KL(symv_tma_launch(a, epi, S, ctx->vt_buf.ptr, ldvt, ctx->stream), "product kernel (TMA)");
     return prof_kind ? prof_end(ctx) : DRSDP_OK;
   }
@@ -257,7 +257,7 @@ static int prof_end(drsdp_ctx *ctx) {
 
 static int run_symv(drsdp_ctx *ctx, SymvArgs &a, int epi, bool gather) {
   return run_product(ctx, a, epi, gather ? MODE2_GATHER : MODE2_NONE, false,
-                     epi == EPI_COSTGRAD ? 1 : epi == EPI_HVP ? 2 : 3);
+                     epi == EPI_COSTGRAD ? 1 : epi == EPI_HVP ? 2 : epi == EPI_BOTH ? 4 : 3);
 }
 
 // ---- generic-p building blocks (p > 64: column-chunked RAW products + row epilogues) ----------
@@ -441,6 +441,40 @@ int eval_fixed(drsdp_ctx *ctx, int flags, int n, int p, const double *M, int64_t
   const bool rows = ctx->sub_rows_mode && M == ctx->sub_M;
   const int r0 = rows ? (int)ctx->sub_row0 : 0;
   const int nloc = rows ? (int)ctx->sub_nloc : n;
+  static const bool no_both = std::getenv("DRSDP_NO_BOTH") != nullptr;
+  if (flags == (DRSDP_EVAL_COSTGRAD | DRSDP_EVAL_HVP) && !no_both && p >= 5 && p <= 32) {
+    // cost + gradient and the HVP along U at the same Y in ONE pass over M: the product M [Y U]
+    // (2p columns) with both row epilogues (EPI_BOTH); falls through when the TMA path is unavailable
+    SymvArgs a = base_symv(ctx, nloc, p, M, ldm);
+    if (rows) a.ncols = n;
+    a.V = Y;
+    a.ldv = ldv;
+    a.Y = Y + (size_t)r0 * ldv;
+    a.ldy = ldv;
+    a.U = U + (size_t)r0 * ldv;
+    a.ldu = ldv;
+    a.V2 = U;  // all rows of U: the second half of the contraction operand [Y U]
+    a.ldv2 = ldv;
+    if (symv_tma_supported(a, EPI_BOTH, MODE2_NONE, false)) {
+      rc = gram(ctx, n, p, Y, ldv, U, G, K, ctx->d_scal + S_GG);
+      if (rc) return rc;
+      a.G = G;
+      a.K = K;
+      a.out = rgrad;
+      a.ldo = ldv;
+      a.egrad = egrad;
+      a.lde = ldv;
+      a.rho_out = rho;
+      a.out2 = hvp;
+      a.ldo2 = ldv;
+      a.scal_out = ctx->d_scal + S_SCAL;
+      a.scal_out2 = ctx->d_scal + S_UH;
+      a.gg = (rows && r0 > 0) ? ctx->d_scal + S_ZERO : ctx->d_scal + S_GG;
+      a.cost_extra = cost_extra_dev;
+      a.cost_out = cost ? cost : ctx->d_scal + S_COST;
+      return run_symv(ctx, a, EPI_BOTH, false);
+    }
+  }
   if (flags & DRSDP_EVAL_COSTGRAD) {
     rc = gram(ctx, n, p, Y, ldv, nullptr, G, nullptr, ctx->d_scal + S_GG);
     if (rc) return rc;
@@ -1078,7 +1112,7 @@ int drsdp_profile_enable(drsdp_ctx *ctx, int enable) {
 }
 
 int drsdp_profile_read(drsdp_ctx *ctx, int32_t kind, double *ms, int64_t *launches) {
-  if (!ctx || kind < 0 || kind > 3) return DRSDP_ERR_INVALID_ARG;
+  if (!ctx || kind < 0 || kind > 4) return DRSDP_ERR_INVALID_ARG;
   if (ctx->sticky) return ctx->sticky;
   CK(cudaStreamSynchronize(ctx->stream), "sync");
   double tot = 0.0;

@@ -64,6 +64,7 @@ enum Slot {
   S_BY = 22,       // 2: b^T y, ||y||^2
   S_YCA = 24,      // 2: yS . cA
   S_ALM = 26,      // 3: ALM assembly sums [sum R^2, <T, S+C>, ||T||^2]
+  S_UH = 29,       // <U, H> of a fused cost+grad+HVP evaluation (EPI_BOTH)
   S_FLAG = 30,     // retraction flag (int stored in a double slot)
   S_ZERO = 31,     // constant 0 (row-block cost: ||G||^2 counted once)
   S_TOTAL = 64

@@ -7,7 +7,10 @@
 
 namespace drsdp {
 
-enum Epi { EPI_RAW = 0, EPI_COSTGRAD = 1, EPI_HVP = 2, EPI_ROWDOT = 3 };
+// EPI_BOTH: one product M [Y U] (V = Y, V2 = U: V^T rows 0..p-1 = Y^T, p..2p-1 = U^T) with the
+// COSTGRAD epilogue on columns [0, p) and the HVP epilogue on columns [p, 2p) of the same row (TMA
+// kernel, 8 < 2p <= 64)
+enum Epi { EPI_RAW = 0, EPI_COSTGRAD = 1, EPI_HVP = 2, EPI_ROWDOT = 3, EPI_BOTH = 4 };
 // second product accumulated into the same tile: none, the ALM gather-product sum_i w[amap_ij] X_i,
 // or a plain second pair A2^T V2 (A2 V2 when ATR)
 enum Mode2 { MODE2_NONE = 0, MODE2_GATHER = 1, MODE2_PAIR = 2 };
@@ -56,6 +59,9 @@ struct SymvArgs {
   int lde = 0;
   double *rho_out = nullptr;  // COSTGRAD, optional
   double *zout = nullptr;     // ROWDOT
+  double *out2 = nullptr;     // BOTH: H (pitch ldo2); scal_out2[0] = <U, H>
+  int ldo2 = 0;
+  double *scal_out2 = nullptr;
   // scalars
   double *tile_scal = nullptr;  // [ntiles][2]
   unsigned *glob_cnt = nullptr;

@@ -310,7 +310,7 @@ bool symm_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
   // p <= 8: measured on B200 (n = 32768) 0.97 ms vs 1.31 ms for the full-matrix kernel; at p = 16 the
   // doubled DMMA work per byte makes this variant DMMA/shared-memory bound (1.69 ms vs 1.37 ms)
   static const bool p16 = std::getenv("DRSDP_SYMM16") != nullptr;  // experiment: p <= 16
-  return mode2 == MODE2_NONE && !atr && a.k == 0 && a.ncols == 0 && a.p <= (p16 ? 16 : 8) && a.A2 == nullptr &&
+  return epi != EPI_BOTH && mode2 == MODE2_NONE && !atr && a.k == 0 && a.ncols == 0 && a.p <= (p16 ? 16 : 8) && a.A2 == nullptr &&
          !(a.lda & 1) && !((uintptr_t)a.A & 15) && tma_encoder() != nullptr && (epi != EPI_RAW || a.p <= 16);
 }
 

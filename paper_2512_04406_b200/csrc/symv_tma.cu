@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
   const int split = blockIdx.y, S = gridDim.y;
   const int c0 = PT * blockIdx.z;
   const int tile = blockIdx.x + gridDim.x * blockIdx.z;
-  const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;
+  const int n = a.n, p = EPI == EPI_RAW ? min(PT, a.p - c0) : a.p;  // EPI_BOTH: 2p columns, p <= PT / 2
   const int j0 = blockIdx.x * BM;
   const int kn = a.ncols > 0 ? a.ncols : n;  // contraction length (row-block mode: all columns)
   const int kpad = (kn + BK - 1) / BK * BK;
@@ -225,6 +225,7 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr) {
   if (mode2 == MODE2_GATHER || atr || a.k > 0) return false;
   if (mode2 == MODE2_PAIR && ((a.lda2 & 1) || ((uintptr_t)a.A2 & 15))) return false;
   if (epi != EPI_RAW && a.p > 64) return false;
+  if (epi == EPI_BOTH && (2 * a.p > 64 || 2 * a.p <= 8 || mode2 != MODE2_NONE || !a.U || !a.V2 || a.A2)) return false;
   if ((a.lda & 1) || ((uintptr_t)a.A & 15)) return false;
   return tma_encoder() != nullptr;
 }
@@ -233,12 +234,9 @@ int symv_tma_rows() { return BM; }
 // column chunk width of the TMA kernel (raw products with p > 64 run in 64-wide chunks: a 128-wide
 // variant, measured on B200 at n = 5051, p = 128 / 512, was no faster — the re-reads of M by the
 // chunks hit L2 — and needs 168 registers with spills at 288 threads)
-int symv_tma_pt(int p, int epi) {
-  (void)epi;
-  return symv_pt(p);
-}
+int symv_tma_pt(int p, int epi) { return symv_pt(epi == EPI_BOTH ? 2 * p : p); }
 int symv_tma_chunks(int p, int epi) { return epi == EPI_RAW ? (p + symv_tma_pt(p, epi) - 1) / symv_tma_pt(p, epi) : 1; }
-int symv_tma_ctas_per_sm(int p) { return symv_pt(p) <= 16 ? 2 : 1; }
+int symv_tma_ctas_per_sm(int pt) { return pt <= 16 ? 2 : 1; }
 int symv_tma_kstep() { return BK; }
 
 template <int PT, int EPI, bool PAIR>
@@ -269,12 +267,15 @@ static cudaError_t tma_dispatch(const SymvArgs &a, int epi, bool pair, const CUt
     case EPI_RAW: return tma_launch_t<PT, EPI_RAW, false>(a, m, S, st);
     case EPI_COSTGRAD: return tma_launch_t<PT, EPI_COSTGRAD, false>(a, m, S, st);
     case EPI_HVP: return tma_launch_t<PT, EPI_HVP, false>(a, m, S, st);
+    case EPI_BOTH:
+      if constexpr (PT >= 16) return tma_launch_t<PT, EPI_BOTH, false>(a, m, S, st);
+      return cudaErrorInvalidValue;
     default: return tma_launch_t<PT, EPI_ROWDOT, false>(a, m, S, st);
   }
 }
 
-// Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR), ldvt = round_up(kn, 2), kn =
-// the contraction length (ncols in row-block mode, else n)
+// Vt: workspace of at least p * ldvt doubles (2 p * ldvt for PAIR and EPI_BOTH), ldvt = round_up(kn, 2),
+// kn = the contraction length (ncols in row-block mode, else n)
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st) {
   const int pt = symv_tma_pt(a.p, epi);
   const bool pair = a.A2 != nullptr;
@@ -284,6 +285,23 @@ cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   double *Vt2 = Vt + (size_t)a.p * ldvt;
+  if (epi == EPI_BOTH) {
+    // rows p .. 2p - 1 of V^T = U^T: one map of 2p rows serves [Y U]
+    transpose_kernel<<<tg, 256, 0, st>>>(kn, a.p, a.V2, a.ldv2, Vt2, ldvt, a.skip);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    CUtensorMap mb[4];
+    if (!make_map(&mb[0], a.A, a.n, kn, a.lda, BM) || !make_map(&mb[1], Vt, 2 * a.p, kn, ldvt, pt))
+      return cudaErrorInvalidValue;
+    mb[2] = mb[0];
+    mb[3] = mb[1];
+    switch (pt) {
+      case 16: return tma_dispatch<16>(a, epi, false, mb, S, st);
+      case 32: return tma_dispatch<32>(a, epi, false, mb, S, st);
+      case 64: return tma_dispatch<64>(a, epi, false, mb, S, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (pair) {
     transpose_kernel<<<tg, 256, 0, st>>>(kn, a.p, a.V2, a.ldv2, Vt2, ldvt, a.skip);
     e = cudaGetLastError();

@@ -150,6 +150,23 @@ def test_fixed_eval_padded_pitch_and_split_calls(ctx, n, p):
     check_fixed(g, o, M, Y)
 
 
+@pytest.mark.parametrize("n,p", [(300, 5), (1000, 16), (4500, 17), (2000, 32)])
+def test_fused_costgrad_hvp_matches_split_calls(ctx, n, p):
+    """COSTGRAD | HVP in one call (5 <= p <= 32) runs one pass over M (the product M [Y U] with both
+    row epilogues, EPI_BOTH); it must agree with the oracle and with two separate calls."""
+    M = sweep_matrix_cpu(n)
+    Y, U = sweep_factor(n, p)
+    fused = gpu_fixed(ctx, M, Y, U, flags=3)
+    split = gpu_fixed(ctx, M, Y, U, flags=0)
+    o = sp.fixed_eval(M, Y, U)
+    check_fixed(fused, o, M, Y)
+    G = Y.T @ Y
+    sE = np.linalg.norm(4 * M @ Y) + np.linalg.norm(4 * Y @ G)
+    for k in ("E", "R", "H"):
+        assert rel(fused[k], split[k], sE) <= 1e-12, k
+    assert abs(fused["f"] - split["f"]) <= 1e-12 * (np.sum(G * G) + np.sum(M * M))
+
+
 def test_fixed_eval_deterministic(ctx):
     n, p = 3000, 16
     M = sweep_matrix_cpu(n)
