@@ -212,3 +212,18 @@ def test_chain_solve_q20_vs_stored_oracle(ctx):
         amaps, cnt, b, _ = sb.relax_chain(Qs, cs)
         _check_certified(Qs, cs, info, sol, amaps, cnt, b)
         assert abs(info["dual_obj"] - g["dual_obj"]) <= 1e-6 * (1 + abs(g["dual_obj"]))
+
+
+def test_chain_solve_paper_size_certified(ctx):
+    """q = 20, t = 20 (the smallest instance of the paper's Table 2): converged, with the
+    residues recomputed by the oracle from the returned tuple and the rounding x_i = sign(y_{x_i})
+    certifying the relaxation value when it is attained (b^T y <= f(x) always, weak duality)."""
+    Qs, cs, info, sol = _gpu_chain_solve(ctx, 20, 20, 0)
+    amaps, cnt, b, _ = sb.relax_chain(Qs, cs)
+    res = _check_certified(Qs, cs, info, sol, amaps, cnt, b)
+    d = 18 * 20 + 2
+    x = np.sign(sol["y"][1:1 + d])
+    x[x == 0] = 1.0
+    fx = sb.chain_value(Qs, cs, x)
+    assert info["dual_obj"] <= fx + 1e-6 * (1 + abs(fx))
+    assert res["eta_max"] <= 1e-8
