@@ -146,7 +146,7 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     for (int s = 1; s <= 64; ++s) {
       const int per = ((ktot + s - 1) / s + bk - 1) / bk * bk;
       if (s > 1 && (int64_t)(s - 1) * per >= ktot) break;
-      const int slots = ctx->num_sms * symv_tma_ctas_per_sm(pt);
+      const int slots = ctx->num_sms * symv_tma_ctas_per_sm(pt, epi);
       const int waves = (ntiles * s + slots - 1) / slots;
       const double cost = (double)waves * (per + 64) + 24.0 * s;
       if (cost < best * 0.999) {

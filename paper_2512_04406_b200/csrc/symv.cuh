@@ -85,7 +85,8 @@ bool symv_tma_supported(const SymvArgs &a, int epi, int mode2, bool atr);
 int symv_tma_rows();
 int symv_tma_pt(int p, int epi);      // column chunk width of the TMA kernel (8 ... 64, 128 for raw p > 64)
 int symv_tma_chunks(int p, int epi);
-int symv_tma_ctas_per_sm(int p);
+int symv_tma_ctas_per_sm(int pt, int epi);
+bool symv_tma_both_duo();
 int symv_tma_kstep();
 cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st);
 // Vt (p x ldvt) = V^T for a k x p row-major V (pitch ldv)

@@ -19,6 +19,8 @@
 // TMA zero-fills out-of-range rows / columns, which handles ragged n and p.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tma.cuh"
 #include "symv.cuh"
@@ -31,16 +33,17 @@ namespace {
 constexpr int BM = 128, BK = 32, NCW = 8;  // rows per CTA, k per stage, consumer warps
 constexpr int NTHREADS = (NCW + 1) * 32;
 
-template <int PT>
+// DUO: two CTAs per SM for PT = 32 (2-stage rings): one CTA's epilogue overlaps the other's stream
+template <int PT, bool DUO = false>
 struct Cfg {
   static constexpr int WC = PT >= 32 ? 2 : 1;  // warps across columns
   static constexpr int WR = NCW / WC;           // warps across rows
   static constexpr int WM = BM / WR, WN = PT / WC;
   static constexpr int JB = WM / 8, CB = WN / 8;
   // PT <= 16: 3 stages so that two CTAs share an SM (one streams while the other runs its epilogue);
-  // PT >= 32: one CTA per SM with a deeper ring
-  static constexpr int CTAS_PER_SM = PT <= 16 ? 2 : 1;
-  static constexpr int STAGES = PT >= 64 ? 3 : (PT <= 16 ? 3 : 4);
+  // PT >= 32: one CTA per SM with a deeper ring (DUO: two CTAs with 2 stages each)
+  static constexpr int CTAS_PER_SM = (PT <= 16 || DUO) ? 2 : 1;
+  static constexpr int STAGES = DUO ? 2 : (PT >= 64 ? 3 : (PT <= 16 ? 3 : 4));
   static constexpr int A_ELEMS = BM * BK, V_ELEMS = PT * BK;
   static constexpr int STAGE_ELEMS = A_ELEMS + V_ELEMS;
   static constexpr uint32_t STAGE_BYTES = STAGE_ELEMS * 8;
@@ -57,11 +60,11 @@ struct Cfg {
 // PAIR: out = M V + A2 V2 as one K-concatenated product [M | A2] [V; V2]; the k-tiles in
 // [0, kpad) come from (tmA, tmV), those in [kpad, 2 kpad) from (tmA2, tmV2), kpad = n rounded up
 // to a multiple of BK (TMA zero-fills the padding columns).
-template <int PT, int EPI, bool PAIR>
-__global__ void __launch_bounds__(NTHREADS, Cfg<PT>::CTAS_PER_SM)
+template <int PT, int EPI, bool PAIR, bool DUO = false>
+__global__ void __launch_bounds__(NTHREADS, Cfg<PT, DUO>::CTAS_PER_SM)
     symv_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmV2, SymvArgs a) {
-  using C = Cfg<PT>;
+  using C = Cfg<PT, DUO>;
   if (a.skip && *(volatile const int *)a.skip) return;
   extern __shared__ unsigned char smem_raw[];
   double *smem = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -236,13 +239,21 @@ int symv_tma_rows() { return BM; }
 // chunks hit L2 — and needs 168 registers with spills at 288 threads)
 int symv_tma_pt(int p, int epi) { return symv_pt(epi == EPI_BOTH ? 2 * p : p); }
 int symv_tma_chunks(int p, int epi) { return epi == EPI_RAW ? (p + symv_tma_pt(p, epi) - 1) / symv_tma_pt(p, epi) : 1; }
-int symv_tma_ctas_per_sm(int pt) { return pt <= 16 ? 2 : 1; }
+// EPI_BOTH at PT = 32 with two CTAs per SM (experiment switch DRSDP_BOTH_DUO=1 / =0)
+bool symv_tma_both_duo() {
+  static const int v = [] {
+    const char *e = std::getenv("DRSDP_BOTH_DUO");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v != 0;
+}
+int symv_tma_ctas_per_sm(int pt, int epi) { return (pt <= 16 || (epi == EPI_BOTH && pt == 32 && symv_tma_both_duo())) ? 2 : 1; }
 int symv_tma_kstep() { return BK; }
 
-template <int PT, int EPI, bool PAIR>
+template <int PT, int EPI, bool PAIR, bool DUO = false>
 static cudaError_t tma_launch_t(const SymvArgs &a, const CUtensorMap *m, int S, cudaStream_t st) {
-  using C = Cfg<PT>;
-  auto k = symv_tma_kernel<PT, EPI, PAIR>;
+  using C = Cfg<PT, DUO>;
+  auto k = symv_tma_kernel<PT, EPI, PAIR, DUO>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
@@ -268,6 +279,9 @@ static cudaError_t tma_dispatch(const SymvArgs &a, int epi, bool pair, const CUt
     case EPI_COSTGRAD: return tma_launch_t<PT, EPI_COSTGRAD, false>(a, m, S, st);
     case EPI_HVP: return tma_launch_t<PT, EPI_HVP, false>(a, m, S, st);
     case EPI_BOTH:
+      if constexpr (PT == 32) {
+        if (symv_tma_both_duo()) return tma_launch_t<PT, EPI_BOTH, false, true>(a, m, S, st);
+      }
       if constexpr (PT >= 16) return tma_launch_t<PT, EPI_BOTH, false>(a, m, S, st);
       return cudaErrorInvalidValue;
     default: return tma_launch_t<PT, EPI_ROWDOT, false>(a, m, S, st);
