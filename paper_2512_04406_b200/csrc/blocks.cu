@@ -288,7 +288,12 @@ cudaError_t blk_makex_launch(int t, int nb, const double *T, int64_t ldt, const 
 // ------------------------------------------------------------------------------------------------
 // block-diagonal product + row epilogue
 // ------------------------------------------------------------------------------------------------
-constexpr int BP_R = 16, BP_J = 32;
+// One CTA per 32-row strip of a block; 8 warps = 4 row groups of 8 rows x 2 column halves. The
+// strip of A (and, for the HVP, the gathered strip W = w[amap]) and the block's rows of V (and X)
+// are staged per 32-wide k-chunk in padded shared memory; every warp runs fp64 DMMA (m8n8k4) on its
+// 8 x PT/2 output slice (2 shared-memory fragment loads per 8 x 8 x 4 step instead of 4 loads per
+// scalar FMA pair), then the shared row epilogue runs on the finished strip.
+constexpr int BP_R = 32, BP_J = 32, BP_LDA = BP_J + 4;
 
 template <int PT, int EPI, bool GATHER>
 __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, int nstrip) {
@@ -296,13 +301,15 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
   extern __shared__ double sm[];
   constexpr bool GSG = PT > 64;  // wide p: G_k, K_k read from global memory in the epilogue
   constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && !GSG;
+  constexpr int LDV = PT + 4;
+  constexpr int NCB = PT / 16;  // 8-column DMMA blocks per warp (each warp owns PT / 2 columns)
   const int p = a.p;
   double *gs = sm;                                        // 2 p^2 (G, K)
   double *ptile = gs + (NEEDG ? 2 * p * p : 0);           // BP_R x PT
-  double *As = ptile + BP_R * PT;                         // BP_R x (BP_J + 1)
-  double *Vs = As + BP_R * (BP_J + 1);                    // BP_J x PT
-  double *Ws = Vs + BP_J * PT;                            // BP_R x (BP_J + 1) (gather)
-  double *Xs = Ws + (GATHER ? BP_R * (BP_J + 1) : 0);     // BP_J x PT (gather)
+  double *As = ptile + BP_R * PT;                         // BP_R x BP_LDA
+  double *Vs = As + BP_R * BP_LDA;                        // BP_J x LDV
+  double *Ws = Vs + BP_J * LDV;                           // BP_R x BP_LDA (gather)
+  double *Xs = Ws + (GATHER ? BP_R * BP_LDA : 0);         // BP_J x LDV (gather)
   __shared__ double scratch[64];
   __shared__ unsigned s_ticket;
   const int tile = blockIdx.x;
@@ -311,44 +318,47 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
   const int li0 = st * BP_R;
   const int rows = min(BP_R, nb - li0);
   const int64_t r0 = b0 + li0;
-  constexpr int QN = BP_R * PT / 256 > 0 ? BP_R * PT / 256 : 1;
-  double acc[QN];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane >> 2, r = lane & 3;
+  const int rg = warp & 3, ch = warp >> 2;
+  const int arow = rg * 8 + q, vcol = ch * (PT / 2) + q;
+  double acc[NCB][2];
 #pragma unroll
-  for (int q = 0; q < QN; ++q) acc[q] = 0.0;
+  for (int cb = 0; cb < NCB; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
   for (int j0 = 0; j0 < nb; j0 += BP_J) {
     const int jn = min(BP_J, nb - j0);
     __syncthreads();
     for (int e = threadIdx.x; e < BP_R * BP_J; e += 256) {
       const int i = e / BP_J, jj = e - i * BP_J;
       const bool ok = i < rows && jj < jn;
-      As[i * (BP_J + 1) + jj] = ok ? a.A[(r0 + i) * a.lda + j0 + jj] : 0.0;
-      if constexpr (GATHER) Ws[i * (BP_J + 1) + jj] = ok ? __ldg(a.w + a.amap[(r0 + i) * a.ldm + j0 + jj]) : 0.0;
+      As[i * BP_LDA + jj] = ok ? a.A[(r0 + i) * a.lda + j0 + jj] : 0.0;
+      if constexpr (GATHER) Ws[i * BP_LDA + jj] = ok ? __ldg(a.w + a.amap[(r0 + i) * a.ldm + j0 + jj]) : 0.0;
     }
     for (int e = threadIdx.x; e < BP_J * PT; e += 256) {
       const int jj = e / PT, c = e - jj * PT;
       const bool ok = jj < jn && c < p;
-      Vs[e] = ok ? a.V[(b0 + j0 + jj) * a.ldv + c] : 0.0;
-      if constexpr (GATHER) Xs[e] = ok ? a.X[(b0 + j0 + jj) * a.ldx + c] : 0.0;
+      Vs[jj * LDV + c] = ok ? a.V[(b0 + j0 + jj) * a.ldv + c] : 0.0;
+      if constexpr (GATHER) Xs[jj * LDV + c] = ok ? a.X[(b0 + j0 + jj) * a.ldx + c] : 0.0;
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int o = threadIdx.x + 256 * q;
-      if (o < BP_R * PT) {
-        const int i = o / PT, c = o - i * PT;
-        double s = acc[q];
-        for (int jj = 0; jj < jn; ++jj) {
-          s = fma(As[i * (BP_J + 1) + jj], Vs[jj * PT + c], s);
-          if constexpr (GATHER) s = fma(Ws[i * (BP_J + 1) + jj], Xs[jj * PT + c], s);
-        }
-        acc[q] = s;
+    for (int kk = 0; kk < BP_J; kk += 4) {
+      const double af = As[arow * BP_LDA + kk + r];
+#pragma unroll
+      for (int cb = 0; cb < NCB; ++cb) dmma_884(acc[cb][0], acc[cb][1], af, Vs[(kk + r) * LDV + vcol + 8 * cb]);
+      if constexpr (GATHER) {
+        const double wf = Ws[arow * BP_LDA + kk + r];
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb) dmma_884(acc[cb][0], acc[cb][1], wf, Xs[(kk + r) * LDV + vcol + 8 * cb]);
       }
     }
   }
+  __syncthreads();
 #pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const int o = threadIdx.x + 256 * q;
-    if (o < BP_R * PT) ptile[o] = acc[q];
+  for (int cb = 0; cb < NCB; ++cb) {
+    const int col = ch * (PT / 2) + 8 * cb + 2 * r;
+    ptile[arow * PT + col] = acc[cb][0];
+    ptile[arow * PT + col + 1] = acc[cb][1];
   }
   SymvArgs al = a;
   if constexpr (EPI == EPI_COSTGRAD || EPI == EPI_HVP) {
@@ -365,8 +375,8 @@ template <int PT, int EPI, bool GATHER>
 static cudaError_t launch_bp(const SymvArgs &a, int t, int nb, cudaStream_t st) {
   constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && PT <= 64;
   const int nstrip = (nb + BP_R - 1) / BP_R;
-  const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * (BP_J + 1) + BP_J * PT +
-                                        (GATHER ? BP_R * (BP_J + 1) + BP_J * PT : 0));
+  const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * BP_LDA + BP_J * (PT + 4) +
+                                        (GATHER ? BP_R * BP_LDA + BP_J * (PT + 4) : 0));
   auto kern = blk_product_kernel<PT, EPI, GATHER>;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

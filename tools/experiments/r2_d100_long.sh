@@ -1,0 +1,8 @@
+# d = 100 (BASELINE configs[2]): three variants run concurrently on the one GPU for up to 55 min each
+mkdir -p gpurun_out
+run() { tag=$1; shift; DRSDP_VERBOSE=1 timeout 3500 python tools/solve_run.py "$@" > gpurun_out/r2L_$tag.log 2> gpurun_out/r2L_$tag.err; }
+run s10 100 3300 4 stall_factor=10.0 &
+run s3 100 3300 4 stall_factor=3.0 &
+run s10t 100 3300 4 stall_factor=10.0 tau2=0.1 &
+wait
+for t in s10 s3 s10t; do echo "== $t"; tail -1 gpurun_out/r2L_$t.log | cut -c1-420; grep "\[drsdp\]" gpurun_out/r2L_$t.err | tail -2 | cut -c1-260; done
