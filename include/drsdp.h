@@ -168,7 +168,7 @@ typedef struct {
   double precond_mu;                   /* truncated-CG preconditioner Prec(R) = P_Y(R W),
                                           W = gbar (Y^T Y + mu gbar I)^{-1}, gbar = tr(Y^T Y)/p
                                           (reading R35); 0 = unpreconditioned; < 0 (default) =
-                                          auto: mu = 0.1 for n >= 2048, none below               */
+                                          auto: mu = 0.1 for 2048 <= n < 8192, none otherwise              */
   int32_t lanczos_steps;               /* block-Lanczos steps per eigen step (block 16), 0 = 40   */
   int32_t reserved;
   double escape_gate;                  /* escape / rank change only when the inner solve ended with

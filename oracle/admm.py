@@ -55,7 +55,7 @@ class Params:
         self.stall_rtr = 10
         self.max_tcg = 100
         self.precond_mu = -1.0  # reading R35: Gram right-preconditioner of the truncated CG (0 = off,
-                                # < 0 = auto: mu = 0.1 for n >= 2048, off below)
+                                # < 0 = auto: mu = 0.1 for 2048 <= n < 8192, off otherwise)
         self.stall_factor = 100.0  # reading R30: the stagnation exit applies within this x the tolerance
         self.escape_gate = 0.0  # reading R36: escape / rank change only after an inner solve within
                                 # escape_gate x its tolerance (0 = always)
@@ -165,7 +165,7 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         Y, info = rtr(prob, Y, RTRParams(n, p, max_iter=prm.max_rtr, rho_reg=prm.rho_reg,
                                         max_tcg=prm.max_tcg if prm.max_tcg > 0 else None,
                                         precond_mu=(prm.precond_mu if prm.precond_mu >= 0 else
-                                                    (0.1 if n >= 2048 else 0.0))), grad_tol, warm_U=U,
+                                                    (0.1 if 2048 <= n < 8192 else 0.0))), grad_tol, warm_U=U,
                       stall=prm.stall_rtr, stall_factor=prm.stall_factor)
         totals["rtr"] += info["iters"]
         totals["tcg"] += info["tcg"]

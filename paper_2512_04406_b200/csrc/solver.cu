@@ -232,12 +232,12 @@ struct Run {
     return DRSDP_OK;
   }
 
-  // reading R35: precond_mu < 0 selects mu = 0.1 for n >= 2048 (measured: d = 80 twice as fast,
-  // d = 40 slower with it) and no preconditioner below
+  // reading R35: precond_mu < 0 selects mu = 0.1 for 2048 <= n < 8192 (measured: d = 80 2.5x faster,
+  // d = 40 slower, d = 150 (n = 11326) not converged after 3360 s with it against 1451 s without)
   // block problems: off (reading R37; the Gram of one block is not the operator of the others)
   double mu() const {
     if (ctx->prob.nblk > 0) return 0.0;
-    return prm.precond_mu >= 0.0 ? prm.precond_mu : (n >= 2048 ? 0.1 : 0.0);
+    return prm.precond_mu >= 0.0 ? prm.precond_mu : (n >= 2048 && n < 8192 ? 0.1 : 0.0);
   }
   bool precond() const { return mu() > 0.0; }
   // W = gbar (G + mu gbar I)^{-1} at the current point: A = G/gbar + mu I (kernel), Cholesky

@@ -24,7 +24,7 @@ LONG = os.environ.get("DRSDP_LONG") == "1"
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not LONG, reason="long solve: set DRSDP_LONG=1")
-@pytest.mark.parametrize("d,kind,limit", [(100, "dense", 3600.0), (150, "er05", 3600.0)])
+@pytest.mark.parametrize("d,kind,limit", [(100, "dense", 3300.0), (150, "er05", 3300.0)])
 def test_long_solve_certified(d, kind, limit):
     from paper_2512_04406_b200 import abi
 
