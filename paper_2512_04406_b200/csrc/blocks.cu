@@ -293,16 +293,22 @@ cudaError_t blk_makex_launch(int t, int nb, const double *T, int64_t ldt, const 
 // are staged per 32-wide k-chunk in padded shared memory; every warp runs fp64 DMMA (m8n8k4) on its
 // 8 x PT/2 output slice (2 shared-memory fragment loads per 8 x 8 x 4 step instead of 4 loads per
 // scalar FMA pair), then the shared row epilogue runs on the finished strip.
-constexpr int BP_R = 32, BP_J = 32, BP_LDA = BP_J + 4;
+constexpr int BP_J = 32, BP_LDA = BP_J + 4;
+// rows per strip: 32 (4 row groups x 2 column halves), 16 at PT = 128 (2 row groups x 4 column
+// quarters) so that two CTAs fit an SM
+template <int PT>
+constexpr int bp_rows() { return PT >= 128 ? 16 : 32; }
 
 template <int PT, int EPI, bool GATHER>
 __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, int nstrip) {
   if (a.skip && *(volatile const int *)a.skip) return;
   extern __shared__ double sm[];
+  constexpr int BP_R = bp_rows<PT>();
+  constexpr int RG = BP_R / 8, CG = 8 / RG;  // warps across rows / columns
   constexpr bool GSG = PT > 64;  // wide p: G_k, K_k read from global memory in the epilogue
   constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && !GSG;
   constexpr int LDV = PT + 4;
-  constexpr int NCB = PT / 16;  // 8-column DMMA blocks per warp (each warp owns PT / 2 columns)
+  constexpr int NCB = PT / (8 * CG);  // 8-column DMMA blocks per warp (each warp owns PT / CG columns)
   const int p = a.p;
   double *gs = sm;                                        // 2 p^2 (G, K)
   double *ptile = gs + (NEEDG ? 2 * p * p : 0);           // BP_R x PT
@@ -320,8 +326,8 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
   const int64_t r0 = b0 + li0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane >> 2, r = lane & 3;
-  const int rg = warp & 3, ch = warp >> 2;
-  const int arow = rg * 8 + q, vcol = ch * (PT / 2) + q;
+  const int rg = warp % RG, ch = warp / RG;
+  const int arow = rg * 8 + q, vcol = ch * (PT / CG) + q;
   double acc[NCB][2];
 #pragma unroll
   for (int cb = 0; cb < NCB; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
   __syncthreads();
 #pragma unroll
   for (int cb = 0; cb < NCB; ++cb) {
-    const int col = ch * (PT / 2) + 8 * cb + 2 * r;
+    const int col = ch * (PT / CG) + 8 * cb + 2 * r;
     ptile[arow * PT + col] = acc[cb][0];
     ptile[arow * PT + col + 1] = acc[cb][1];
   }
@@ -369,11 +375,12 @@ __global__ void __launch_bounds__(256) blk_product_kernel(SymvArgs a, int nb, in
   tile_epilogue<PT, EPI, BP_R, 256, GSG>(al, ptile, gs, scratch, &s_ticket, tile, (int)r0, 0, (int)(b0 + nb), p);
 }
 
-int blk_product_tiles(int t, int nb) { return t * ((nb + BP_R - 1) / BP_R); }
+int blk_product_tiles(int t, int nb) { return t * ((nb + 15) / 16); }  // upper bound over the strip heights
 
 template <int PT, int EPI, bool GATHER>
 static cudaError_t launch_bp(const SymvArgs &a, int t, int nb, cudaStream_t st) {
   constexpr bool NEEDG = (EPI == EPI_COSTGRAD || EPI == EPI_HVP) && PT <= 64;
+  constexpr int BP_R = bp_rows<PT>();
   const int nstrip = (nb + BP_R - 1) / BP_R;
   const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * BP_LDA + BP_J * (PT + 4) +
                                         (GATHER ? BP_R * BP_LDA + BP_J * (PT + 4) : 0));
