@@ -77,10 +77,11 @@ cudaError_t blk_gram_launch(int t, int nb, int p, const double *Y, int ldy, cons
   if (p > kBlkMaxP) return cudaErrorInvalidValue;
   const int rows = bg_rows(nb, p, U != nullptr);
   const size_t smem = sizeof(double) * rows * p * (U ? 2 : 1);
-  if (smem > 48 * 1024) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(blk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attr = false;  // bg_rows keeps the staging <= 64 KB: opt in once
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(blk_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
     if (e != cudaSuccess) return e;
+    attr = true;
   }
   const dim3 grid(t, (p * p + 256 * BG_MAXO - 1) / (256 * BG_MAXO));
   blk_gram_kernel<<<grid, 256, smem, st>>>(nb, p, Y, ldy, U, ldu, G, K, skip, rows);
@@ -385,9 +386,11 @@ static cudaError_t launch_bp(const SymvArgs &a, int t, int nb, cudaStream_t st) 
   const size_t smem = sizeof(double) * ((NEEDG ? 2 * a.p * a.p : 0) + BP_R * PT + BP_R * BP_LDA + BP_J * (PT + 4) +
                                         (GATHER ? BP_R * BP_LDA + BP_J * (PT + 4) : 0));
   auto kern = blk_product_kernel<PT, EPI, GATHER>;
-  if (smem > 48 * 1024) {
+  static size_t attr_smem = 0;  // per instantiation: opt in once for the largest size seen
+  if (smem > 48 * 1024 && smem > attr_smem) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    attr_smem = smem;
   }
   kern<<<t * nstrip, 256, smem, st>>>(a, nb, nstrip);
   return cudaGetLastError();

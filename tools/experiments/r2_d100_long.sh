@@ -1,5 +1,7 @@
 # d = 100 (BASELINE configs[2]): three variants run concurrently on the one GPU for up to 55 min each
 mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_blocks.py -x -q > gpurun_out/r2L_blocks.log 2>&1; tail -1 gpurun_out/r2L_blocks.log
+timeout 300 python tools/alm_profile.py chain:20:120 16,64,128 30 2>&1 | tail -3
 run() { tag=$1; shift; DRSDP_VERBOSE=1 timeout 3500 python tools/solve_run.py "$@" > gpurun_out/r2L_$tag.log 2> gpurun_out/r2L_$tag.err; }
 run s10 100 3300 4 stall_factor=10.0 &
 run s3 100 3300 4 stall_factor=3.0 &
