@@ -311,6 +311,22 @@ def timed_evals(ctx, stream, torch, n, p, Md, Yd, Ud, reps, warmup, flush=None):
             b.synchronize()
             tot += a.elapsed_time(b)
         res[name] = tot / reps
+    if 5 <= p <= 32:
+        # the fused one-pass call (cost+grad and HVP at the same Y): device ms per call
+        for w in range(warmup):
+            ctx.subproblem_eval(3, p, Yd, Ud, cost, None, R, H)
+        tot = 0.0
+        for r in range(reps):
+            if flush is not None:
+                flush_sink.copy_(flush.sum())
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.subproblem_eval(3, p, Yd, Ud, cost, None, R, H)
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        res["both"] = tot / reps
     return res
 
 
@@ -475,6 +491,18 @@ def run_gpu(args):
                     t_roof_alg = max(by / (hbm * 1e9), fl / (f64 * 1e12))
                     sweep.append({"n": sn, "p": sp_, "eval": kind, "us": ms[kind] * 1e3, "evals_per_s": 1.0 / t,
                                   "gbs_8n2": 8.0 * sn * sn / t / 1e9, "tflops": fl / t / 1e12,
+                                  "frac_bj5_roofline": t_roof / t, "frac_alg_roofline": t_roof_alg / t})
+                if "both" in ms:
+                    # one call = 2 evaluations: M once, both operand sets, both evaluations' flops
+                    b_cg, f_cg = work_units(sn, sp_, "costgrad")
+                    b_hv, f_hv = work_units(sn, sp_, "hvp")
+                    by = b_cg + b_hv - work_units(sn, sp_, "matrix")[0]
+                    fl = f_cg + f_hv
+                    t = ms["both"] / 1e3
+                    t_roof = 2.0 * max(8.0 * sn * sn / (hbm * 1e9), 2.0 * sn * sn * sp_ / (f64 * 1e12))
+                    t_roof_alg = max(by / (hbm * 1e9), fl / (f64 * 1e12))
+                    sweep.append({"n": sn, "p": sp_, "eval": "costgrad+hvp (one call, one pass over M)",
+                                  "us": ms["both"] * 1e3, "evals_per_s": 2.0 / t, "tflops": fl / t / 1e12,
                                   "frac_bj5_roofline": t_roof / t, "frac_alg_roofline": t_roof_alg / t})
             del Ms
             torch.cuda.empty_cache()
