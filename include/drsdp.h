@@ -170,12 +170,18 @@ typedef struct {
                                           (reading R35); 0 = unpreconditioned; < 0 (default) =
                                           auto: mu = 0.1 for 2048 <= n < 8192, none otherwise              */
   int32_t lanczos_steps;               /* block-Lanczos steps per eigen step (block 16), 0 = 40   */
-  int32_t reserved;
+  int32_t hold_max;                    /* multiplier hold (reading R40): at most this many consecutive
+                                          outer iterations may keep X~ (0 = never hold)               */
   double escape_gate;                  /* escape / rank change only when the inner solve ended with
                                           ||grad|| <= escape_gate x its tolerance (reading R36);
                                           0 = always                                               */
   double stall_factor;                 /* the stagnation exit (stall_rtr) applies only within
                                           stall_factor x the inner tolerance (reading R30; default 100) */
+  double hold_tau;                     /* multiplier hold (reading R40, the subproblem stopping rule
+                                          lambda_min(X^{k+1}) >= -tau_k of Thm 5.3): when
+                                          eta_d(X^{k+1}) > hold_tau min(1, eta_p) and X^{k+1} has escape
+                                          directions, the X~ update is undone, sigma kept, and the
+                                          same subproblem is re-solved from the escaped point; 0 = off */
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);
@@ -210,7 +216,7 @@ int drsdp_get_solution(drsdp_ctx *ctx, double *y, double *Y, int32_t *p, double 
 
 /* Per-outer-iteration trace, 13 doubles per row in the order
  * iter, eta_p, eta_d, eta_g, eta_max, primal_obj, dual_obj, sigma, p, inner_iters, cg_iters,
- * escape_delta, time_s.  Copies min(max_rows, available) rows; *n_rows = rows available. */
+ * escape_delta (negative: a held multiplier, reading R40), time_s.  Copies min(max_rows, available) rows; *n_rows = rows available. */
 int drsdp_get_trace(drsdp_ctx *ctx, int32_t max_rows, double *rows, int32_t *n_rows);
 
 /* ---------------------------------------------------------------------------------------------

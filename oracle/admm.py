@@ -59,6 +59,9 @@ class Params:
         self.stall_factor = 100.0  # reading R30: the stagnation exit applies within this x the tolerance
         self.escape_gate = 0.0  # reading R36: escape / rank change only after an inner solve within
                                 # escape_gate x its tolerance (0 = always)
+        self.hold_max = 0  # reading R40: at most this many consecutive multiplier holds (0 = never)
+        self.hold_tau = 0.0  # reading R40: hold while eta_d(X^{k+1}) > hold_tau min(1, eta_p) (Thm 5.3's
+                             # lambda_min(X^{k+1}) >= -tau_k, enforced by escapes)
         for k, v in kw.items():
             if not hasattr(self, k):
                 raise TypeError(f"unknown parameter {k}")
@@ -151,6 +154,7 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
     status = "not_converged"
     res = None
     totals = {"rtr": 0, "tcg": 0, "costgrad": 0, "hvp": 0, "p_max": Y.shape[1]}
+    holds = 0
     for k in range(prm.max_outer):
         p = Y.shape[1]
         if prm.mode == "alm":
@@ -176,6 +180,7 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         y = ops.y_update(amap, cnt, S, C)
         SC = S if C is None else S + C
         Rp = ops.At(amap, y) - SC
+        T_prev = T
         T = T - sigma * Rp
         res = residues(amap, cnt, b, C, y, Y, T)
         if callback is not None:
@@ -202,6 +207,11 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         gated = prm.escape_gate > 0 and info["gnorm"] > prm.escape_gate * grad_tol
         if gated:
             Vs = None
+        # multiplier hold (reading R40): X^{k+1} = grad Phi_k(S^{k+1}) - Diag(z) is subproblem k's
+        # certificate (Lemma 3.2, Prop 4.3); while it has escape directions and
+        # eta_d > hold_tau min(1, eta_p), undo step 6, keep sigma, escape and re-solve subproblem k
+        hold = (prm.hold_max > 0 and prm.hold_tau > 0 and holds < prm.hold_max and Vs is not None
+                and res["eta_d"] > prm.hold_tau * min(1.0, res["eta_p"]))
         # rank tolerance tied to the residual (reading R32); no reduction in an iteration that
         # escapes (reading R34: the escape columns of the previous iteration are O(sqrt(|lambda|/sigma))
         # and a relative tolerance would remove them before they grow)
@@ -215,6 +225,14 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
         else:
             U = None
         totals["p_max"] = max(totals["p_max"], Y.shape[1])
+        if hold:
+            T = T_prev
+            holds += 1
+            row["escape_delta"] = -delta  # negative: the multiplier was held
+            row["time_s"] = time.perf_counter() - t0
+            trace.append(row)
+            continue
+        holds = 0
         sigma_new = sigma_update(sigma, float(np.linalg.norm(Rp)), b_norm, grad_paper, prm)
         row["escape_delta"] = delta
         row["time_s"] = time.perf_counter() - t0

@@ -54,6 +54,7 @@ struct SolverState {
   DBuf<double> Ybuf[2], Rbuf[2], Mbuf[2], Gbuf[2], rhobuf[2], ySbuf[2], Dbuf[2], Zbuf;
   DBuf<double> eta, eta2, Heta, Heta2, r, r2, delta, Hdelta, Uw, tmp, K, wZ;
   DBuf<double> T, X, W, ystar, z, Vst, Wsmall, Geig, Gw;
+  DBuf<double> Tsave;  // X~^k + D kept while a multiplier hold is possible (reading R40)
   DBuf<double> Apre, Wpre, pwork;  // tCG preconditioner (reading R35): A = G/gbar + mu I, W = A^{-1}
   LanczosWork lz;                  // block Lanczos eigen step (lanczos.cu)
   DBuf<int> devinfo;
@@ -97,7 +98,7 @@ void free_solver(drsdp_ctx *ctx) {
   s->Zbuf.release();
   DBuf<double> *bs[] = {&s->eta, &s->eta2, &s->Heta, &s->Heta2, &s->r, &s->r2, &s->delta, &s->Hdelta, &s->Uw,
                         &s->tmp, &s->K, &s->wZ, &s->T, &s->X, &s->W, &s->ystar, &s->z, &s->Vst, &s->Wsmall,
-                        &s->work, &s->Geig, &s->Gw, &s->gwork, &s->Apre, &s->Wpre, &s->pwork};
+                        &s->work, &s->Geig, &s->Gw, &s->gwork, &s->Apre, &s->Wpre, &s->pwork, &s->Tsave};
   for (auto *b : bs) b->release();
   s->devinfo.release();
   s->lz.release();
@@ -666,6 +667,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   int status = DRSDP_ERR_NOT_CONVERGED;
   double eta_p = 0, eta_d = 0, eta_g = 0, dobj = 0, pobj = 0;
   int outer = 0;
+  int holds = 0;  // consecutive multiplier holds (reading R40)
   std::vector<double> lam(n);
   for (int k = 0; k < prm.max_outer; ++k) {
     outer = k + 1;
@@ -723,6 +725,15 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     } else {
       CK(cudaMemcpyAsync(s->ystar.ptr, s->cur.yS, sizeof(double) * P.m, cudaMemcpyDeviceToDevice, ctx->stream),
          "copy y");
+    }
+    // multiplier hold (reading R40): keep X~^k + D so that the update below can be undone when
+    // X^{k+1} shows that subproblem k is not yet solved to lambda_min >= -tau_k (Thm 5.3)
+    const bool can_hold = prm.hold_max > 0 && prm.hold_tau > 0.0 && holds < prm.hold_max;
+    if (can_hold) {
+      CK(s->Tsave.ensure((size_t)n * P.ld), "alloc T copy");
+      CK(cudaMemcpyAsync(s->Tsave.ptr, s->T.ptr, sizeof(double) * (size_t)n * P.ld, cudaMemcpyDeviceToDevice,
+                         ctx->stream),
+         "save T");
     }
     // T <- T - sigma (A*(y) - S - C)
     DualArgs da;
@@ -885,6 +896,10 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     // no reduction)
     const bool gated = prm.escape_gate > 0.0 && s->cur.gn > prm.escape_gate * grad_tol;
     if (gated) dv = 0;
+    // multiplier hold (reading R40): subproblem k's certificate X^{k+1} = grad Phi_k(S^{k+1}) - Diag(z)
+    // still has escape directions with eta_d above hold_tau min(1, eta_p): undo the X~ update, keep
+    // sigma, escape, and re-solve subproblem k (at most hold_max times in a row)
+    const bool hold = can_hold && dv > 0 && eta_d > prm.hold_tau * std::min(1.0, eta_p);
     // rank reduction (readings R15, R32, R34): only in an iteration that does not escape, compress
     // Y to its numerical rank at the tolerance rank_tol_k = min(rank_tol, max(1e-8, 0.01 sqrt(eta_max))).
     // Eigenpairs of the p x p Gram matrix G = Y^T Y (cuSOLVER dsyevd; G is symmetric so
@@ -972,6 +987,18 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       warm = false;
     }
     p_max = std::max(p_max, p);
+    if (hold && !(prm.time_limit_s > 0 && now_s() - t0 > prm.time_limit_s)) {
+      CK(cudaMemcpyAsync(s->T.ptr, s->Tsave.ptr, sizeof(double) * (size_t)n * P.ld, cudaMemcpyDeviceToDevice,
+                         ctx->stream),
+         "restore T");
+      ++holds;
+      row[11] = -dv;  // trace: a negative escape_delta marks a held multiplier
+      row[12] = now_s() - t0;
+      ctx->trace.insert(ctx->trace.end(), row, row + 13);
+      if (verbose) std::fprintf(stderr, "[drsdp] k=%d hold %d (multiplier kept, %d escape columns)\n", k + 1, holds, dv);
+      continue;
+    }
+    holds = 0;
     // sigma update, Eq. 5.1
     const double ratio = R_norm / (1.0 + b_norm);
     double sig = run.sigma;
