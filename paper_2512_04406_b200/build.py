@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdrsdp.so")
-SOURCES = ["abi.cu", "solver.cu", "symv.cu", "symv_tma.cu", "symv_symm.cu", "gram_tile.cu", "kernels.cu", "lanczos.cu",
+SOURCES = ["abi.cu", "solver.cu", "symv.cu", "symv_tma.cu", "symv_gather.cu", "symv_symm.cu", "gram_tile.cu", "kernels.cu", "lanczos.cu",
            "blocks.cu"]
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 CUDA_HOME = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))

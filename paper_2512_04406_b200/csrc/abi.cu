@@ -87,6 +87,44 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
   if (a.ncols > 0 && a.ncols != a.n && (no_tma || !symv_tma_supported(a, epi, mode2, atr)))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG,
                      "row-block product needs the TMA kernel (even pitch, 16 B aligned rows, p <= 64)");
+  // matrix-light gather-product (f1): A*(w) gathered inside the ring from the TMA-loaded index-map panel;
+  // fused HVP epilogue for p <= 64 (DRSDP_FUSED_GATHER=0: off, =2: also the raw column chunks of p > 64)
+  static const int fused_gather = [] {
+    const char *e = std::getenv("DRSDP_FUSED_GATHER");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!no_tma && fused_gather && mode2 == MODE2_GATHER && a.n >= 2048 && (epi == EPI_HVP || fused_gather >= 2) &&
+      symv_gather_supported(a, epi, atr)) {
+    const int pt = symv_tma_pt(a.p, epi), bm = symv_tma_rows(), bk = symv_gather_kstep();
+    const int ntiles = ((a.n + bm - 1) / bm) * symv_tma_chunks(a.p, epi);
+    int S = 1;
+    double best = 1e300;
+    for (int s = 1; s <= 64; ++s) {
+      const int per = ((a.n + s - 1) / s + bk - 1) / bk * bk;
+      if (s > 1 && (int64_t)(s - 1) * per >= a.n) break;
+      const int waves = (ntiles * s + ctx->num_sms - 1) / ctx->num_sms;
+      const double cost = (double)waves * (2 * per + 64) + 24.0 * s;
+      if (cost < best * 0.999) {
+        best = cost;
+        S = s;
+      }
+    }
+    a.rows_per_split = ((a.n + S - 1) / S + bk - 1) / bk * bk;
+    if (S > 1) CK(ctx->symv_part.ensure((size_t)ntiles * S * bm * pt), "alloc split workspace");
+    CK(ctx->tile_cnt.ensure_zeroed((size_t)ntiles), "alloc tile counters");
+    CK(ctx->tile_scal.ensure((size_t)ntiles * 3), "alloc tile scalars");
+    const int64_t ldvt = (a.n + 1) / 2 * 2;
+    CK(ctx->vt_buf.ensure((size_t)2 * a.p * ldvt), "alloc V^T");
+    a.part = ctx->symv_part.ptr;
+    a.tile_cnt = ctx->tile_cnt.ptr;
+    a.tile_scal = ctx->tile_scal.ptr;
+    a.glob_cnt = ctx->counters + C_SYMV;
+    int rc = prof_kind ? prof_begin(ctx, prof_kind) : DRSDP_OK;
+    if (rc) return rc;
+    ctx->launches += 2;  // transposes
+    KL(symv_gather_launch(a, epi, S, ctx->vt_buf.ptr, ldvt, ctx->stream), "product kernel (TMA, fused gather)");
+    return prof_kind ? prof_end(ctx) : DRSDP_OK;
+  }
   // (small n keeps the register-direct gather kernel: one launch instead of assembly + product)
   if (!no_tma && mode2 == MODE2_GATHER && !atr && a.n >= 2048 && (a.lda % 2) == 0 && ((uintptr_t)a.A & 15) == 0 &&
       (a.k == 0 || a.k == a.n)) {

@@ -93,6 +93,14 @@ cudaError_t symv_tma_launch(const SymvArgs &a, int epi, int S, double *Vt, int64
 cudaError_t symv_transpose(int k, int p, const double *V, int ldv, double *Vt, int64_t ldvt, const int *skip,
                            cudaStream_t st);
 
+// Matrix-light ALM gather-product (symv_gather.cu): out = M V + A*(w) X with A*(w) gathered
+// from w through the TMA-loaded index-map panel inside the ring (never materialised); a.V = U, a.X = Y,
+// a.amap / a.ldm / a.w as for MODE2_GATHER. EPI_HVP (p <= 64) or EPI_RAW (column chunks on grid z).
+// Vt: 2 p ldvt doubles, ldvt = round_up(n, 2). Split-K in multiples of symv_gather_kstep() columns.
+bool symv_gather_supported(const SymvArgs &a, int epi, bool atr);
+int symv_gather_kstep();
+cudaError_t symv_gather_launch(const SymvArgs &a, int epi, int S, double *Vt, int64_t ldvt, cudaStream_t st);
+
 // Upper-triangle ("symmetric half") variant (symv_symm.cu) for p <= 16: a partial-product kernel
 // over runs of 128 x 128 upper tiles and a reduce + row-epilogue kernel (one CTA per 128 rows).
 // symm_units fills the unit table (int4 {I, Ja, Jb, 0} per unit) and the per-block-row start

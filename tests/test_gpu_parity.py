@@ -415,11 +415,13 @@ def _state_vectorised_map(d, kind, seed, sigma, p):
     return Q, c, amap, cnt, b, T, Y, U
 
 
-@pytest.mark.parametrize("d,p", [(40, 24), (100, 40), (100, 96), (100, 256), (100, 512), (100, 1024), (150, 64)])
+@pytest.mark.parametrize("d,p", [(40, 24), (70, 6), (70, 16), (100, 8), (100, 30), (100, 40), (100, 96), (100, 256),
+                                 (100, 512), (100, 1024), (150, 64)])
 def test_alm_eval_full_size(ctx, d, p):
     """BASELINE configs[1]/[2]/[3] sizes (n = 821, 5051, 11326): the y-eliminated evaluation in the
-    solver's launch configuration (dense Gram tiles + TMA products; p > 64 column-chunked products
-    and row epilogues up to DRSDP_MAX_P) against the oracle."""
+    solver's launch configuration (dense Gram tiles + TMA products; for n >= 2048 and p <= 64 the
+    matrix-light HVP product of symv_gather.cu — every tile width 8 / 16 / 32 / 64, ragged n and p;
+    p > 64 column-chunked products and row epilogues up to DRSDP_MAX_P) against the oracle."""
     from paper_2512_04406_b200 import abi
 
     if d == 150:
