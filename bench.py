@@ -11,7 +11,7 @@ value = evaluations/s (whole job; 2 per step). The other sweep points (n in {409
 p in {8, 16, 32, 64}) and full ManiDSDP solves of the dense BQPs d = 10, 40 (configs[0..1], "solve time to
 KKT 1e-8") and d = 80 (the paper's largest dense size) are reported in the same JSON line under "sweep" and "solves".
 
-Multi-GPU (--gpus N under torchrun): the subproblem does not shard in this round (DESIGN.md
+Multi-GPU (--gpus N under torchrun): the benchmark runs replicas (no data-path collective, DESIGN.md
 "replicas only"): every rank runs the same workload on its own GPU, no collective on the data
 path; value = all ranks' evaluations / max-over-ranks time (weak scaling).
 
