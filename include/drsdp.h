@@ -39,8 +39,10 @@ typedef struct drsdp_ctx drsdp_ctx; /* opaque; owns every device buffer it alloc
 
 /* Largest factor width p accepted anywhere (evaluations, initial factor, solver rank growth).
  * p <= 64 runs the fused single-pass kernels; 64 < p <= DRSDP_MAX_P runs the product kernel in
- * column chunks of 64 followed by separate row-epilogue kernels (same arithmetic). */
-#define DRSDP_MAX_P 1024
+ * column chunks of 64 followed by separate row-epilogue kernels (same arithmetic). The solver's rank
+ * growth (escape columns) stops at min(DRSDP_MAX_P, n): at d = 100 the cap 1024 of round 1
+ * was reached while X still had ~1000 negative eigenvalues, hence 4096. */
+#define DRSDP_MAX_P 4096
 
 typedef enum {
   DRSDP_OK = 0,

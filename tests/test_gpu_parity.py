@@ -108,9 +108,9 @@ def test_fixed_eval_upper_triangle_path(ctx, n, p):
     check_fixed(g, sp.fixed_eval(M, Y, U), M, Y)
 
 
-@pytest.mark.parametrize("n,p", [(1, 1), (2, 3), (5, 64), (64, 1024), (300, 1024)])
+@pytest.mark.parametrize("n,p", [(1, 1), (2, 3), (5, 64), (64, 1024), (300, 1024), (300, 2048), (130, 4096)])
 def test_fixed_eval_degenerate_and_max_p(ctx, n, p):
-    """Degenerate sizes (n = 1, p > n) and the largest factor width DRSDP_MAX_P = 1024."""
+    """Degenerate sizes (n = 1, p > n) and the largest factor width DRSDP_MAX_P = 4096."""
     M = sweep_matrix_cpu(n) if n > 1 else np.array([[0.7]])
     Y, U = sweep_factor(n, p)
     g = gpu_fixed(ctx, M, Y, U)
@@ -126,7 +126,7 @@ def test_abi_argument_and_state_errors(ctx):
     Y, U = sweep_factor(n, 4)
     Yd, Ud = dev(Y), dev(U)
     H = torch.empty_like(Yd)
-    for bad_p in (0, 1025):
+    for bad_p in (0, 4097):
         with pytest.raises(abi.DrsdpError) as e:
             ctx.subproblem_eval(abi.EVAL_COSTGRAD, bad_p, Yd, None, None, None, H, None)
         assert e.value.code == abi.ERR_INVALID_ARG
@@ -416,7 +416,7 @@ def _state_vectorised_map(d, kind, seed, sigma, p):
 
 
 @pytest.mark.parametrize("d,p", [(40, 24), (70, 6), (70, 16), (100, 8), (100, 30), (100, 40), (100, 96), (100, 256),
-                                 (100, 512), (100, 1024), (150, 64)])
+                                 (100, 512), (100, 1024), (70, 1536), (70, 2048), (150, 64)])
 def test_alm_eval_full_size(ctx, d, p):
     """BASELINE configs[1]/[2]/[3] sizes (n = 821, 5051, 11326): the y-eliminated evaluation in the
     solver's launch configuration (dense Gram tiles + TMA products; for n >= 2048 and p <= 64 the
