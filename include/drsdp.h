@@ -184,6 +184,10 @@ typedef struct {
                                           eta_d(X^{k+1}) > hold_tau min(1, eta_p) and X^{k+1} has escape
                                           directions, the X~ update is undone, sigma kept, and the
                                           same subproblem is re-solved from the escaped point; 0 = off */
+  double sigma_boost;                  /* penalty boost (reading R41; Alg. 1 step 8 "certain policy",
+                                          P:190): when eta_d <= sigma_boost * eta_p the dual side is
+                                          ahead of the primal one and sigma_{k+1} = min(gamma sigma_k,
+                                          sigma_max) whatever Eq. 5.1 says; 0 = off (Eq. 5.1 alone)  */
 } drsdp_params;
 
 int drsdp_default_params(drsdp_params *out);
@@ -224,7 +228,7 @@ int drsdp_get_trace(drsdp_ctx *ctx, int32_t max_rows, double *rows, int32_t *n_r
 /* ---------------------------------------------------------------------------------------------
  * Subproblem evaluation (north-star kernels (b)+(c); bench and parity path)
  *
- * Fixed-M subproblem f(Y) = ||Y Y^T - M||_F^2 on the oblique manifold (Sub-k, P:199-208, with
+ * Fixed-M subproblem f(Y) = ||Y Y^T - M||_F^2 on the oblique manifold (Sub-k, P:190-208, with
  * M = A*(y) - C - (X~ + D)/sigma: L_sigma = (sigma/2) f + const). Outputs on the f scale:
  *   cost   f
  *   egrad  E = 4 (Y Y^T Y - M Y)                 (Euclidean gradient)

@@ -62,6 +62,8 @@ class Params:
         self.hold_max = 0  # reading R40: at most this many consecutive multiplier holds (0 = never)
         self.hold_tau = 0.0  # reading R40: hold while eta_d(X^{k+1}) > hold_tau min(1, eta_p) (Thm 5.3's
                              # lambda_min(X^{k+1}) >= -tau_k, enforced by escapes)
+        self.sigma_boost = 0.0  # reading R41: when eta_d <= sigma_boost * eta_p, sigma_{k+1} = min(gamma sigma_k,
+                                # sigma_max) whatever Eq. 5.1 says (Alg. 1 step 8 "certain policy"); 0 = off
         for k, v in kw.items():
             if not hasattr(self, k):
                 raise TypeError(f"unknown parameter {k}")
@@ -234,6 +236,8 @@ def solve(amap, cnt, b, C, prm: Params, Y0: np.ndarray, verbose=False, callback=
             continue
         holds = 0
         sigma_new = sigma_update(sigma, float(np.linalg.norm(Rp)), b_norm, grad_paper, prm)
+        if prm.sigma_boost > 0 and res["eta_d"] <= prm.sigma_boost * res["eta_p"]:
+            sigma_new = min(prm.gamma * sigma, prm.sigma_max)  # reading R41
         row["escape_delta"] = delta
         row["time_s"] = time.perf_counter() - t0
         trace.append(row)

@@ -42,7 +42,8 @@ class Params(C.Structure):
                 ("escape_max", C.c_int32), ("mode", C.c_int32), ("seed", C.c_uint64), ("rho_reg", C.c_double),
                 ("stall_rtr", C.c_int32), ("eig_method", C.c_int32), ("precond_mu", C.c_double),
                 ("lanczos_steps", C.c_int32), ("hold_max", C.c_int32),
-                ("escape_gate", C.c_double), ("stall_factor", C.c_double), ("hold_tau", C.c_double)]
+                ("escape_gate", C.c_double), ("stall_factor", C.c_double), ("hold_tau", C.c_double),
+                ("sigma_boost", C.c_double)]
 
 
 class Info(C.Structure):

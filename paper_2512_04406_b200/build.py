@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     lib64 = os.path.join(CUDA_HOME, "lib64")
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
-           f"-L{lib64}", "-lcusolver", "-lcudart", f"-Xlinker=-rpath,{lib64}"]
+           f"-L{lib64}", "-lcusolver", "-lcudart", "-ldl", f"-Xlinker=-rpath,{lib64}"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

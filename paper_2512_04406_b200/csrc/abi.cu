@@ -1441,6 +1441,7 @@ int drsdp_default_params(drsdp_params *o) {
   o->escape_gate = 0.0;
   o->hold_max = 0;
   o->hold_tau = 0.0;
+  o->sigma_boost = 0.0;
   return DRSDP_OK;
 }
 
@@ -1451,7 +1452,7 @@ int drsdp_set_params(drsdp_ctx *ctx, const drsdp_params *prm) {
         q.tau2 >= q.tau1 && q.tol > 0 && q.p0 >= 1 && q.p0 <= DRSDP_MAX_P && q.max_outer >= 1 && q.max_rtr >= 1 &&
         q.escape_max >= 0 && (q.mode == 0 || q.mode == 1) && q.rank_tol > 0 && q.eig_neg_tol >= 0 &&
         q.rho_reg >= 0 && q.stall_rtr >= 0 && q.stall_factor > 0 && q.eig_method >= 0 && q.eig_method <= 2 &&
-        q.escape_gate >= 0 && q.hold_max >= 0 && q.hold_tau >= 0))
+        q.escape_gate >= 0 && q.hold_max >= 0 && q.hold_tau >= 0 && q.sigma_boost >= 0))
     return set_error(ctx, DRSDP_ERR_INVALID_ARG, "set_params: parameter out of range");
   ctx->prm = q;
   return DRSDP_OK;

@@ -22,6 +22,7 @@
 #include "lanczos.cuh"
 #include "blocks.cuh"
 #include "symv.cuh"
+#include "nvtx_ranges.h"
 
 namespace drsdp {
 
@@ -128,6 +129,7 @@ struct Run {
   int64_t costgrad = 0, hvp = 0, rtr_total = 0, tcg_total = 0, lz_steps = 0;
 
   int costgrad_at(Point &P, int p) {
+    NvtxRange nv("drsdp:costgrad");
     ++costgrad;
     RC(alm_or_fixed_costgrad(P, p));
     RC(read_scalars(ctx, S_COST, 4));
@@ -258,6 +260,7 @@ struct Run {
   }
 
   int tcg(int p, double Delta, int max_tcg) {
+    NvtxRange nv("drsdp:tcg");
     Point &C = s->cur;
     const size_t bytes = (size_t)n * s->ldp * 8;
     CK(cudaMemsetAsync(s->eta.ptr, 0, bytes, ctx->stream), "memset");
@@ -339,6 +342,7 @@ struct Run {
   int last_exit = 0;  // 0 gradient tolerance, 1 stagnation, 2 max_rtr, 3 tiny radius
   double last_warm_t = -1.0, last_gn0 = 0.0;
   int rtr(int p, double grad_tol, bool warm, int &iters_out, int &tcg_out) {
+    NvtxRange nv("drsdp:rtr");
     RC(costgrad_at(s->cur, p));
     last_warm_t = -1.0;
     if (warm) {
@@ -671,6 +675,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
   std::vector<double> lam(n);
   for (int k = 0; k < prm.max_outer; ++k) {
     outer = k + 1;
+    NvtxPhase phase;  // NVTX: inner solve / multiplier update / eigen step / rank update
+    phase.set("drsdp:outer/inner_solve");
     if (prm.mode == 1) {
       // fixed-M: M = A*(y^k) - C - T/sigma and ||M||^2 as the cost constant
       AssembleArgs as;
@@ -701,6 +707,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     run.rtr_total += rtr_it;
     run.tcg_total += tcg_it;
     const double grad_paper = 0.5 * run.sigma * s->cur.gn;
+    phase.set("drsdp:outer/multiplier_update");
     // y^{k+1} = y(S^{k+1})
     if (prm.mode == 1) {
       SegArgs sg;
@@ -761,6 +768,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
     KL(vdot_launch(P.m, s->ystar.ptr, P.b.ptr, ctx->red_part.ptr, ctx->counters + C_DOT, ctx->d_scal + S_BY,
                    ctx->stream),
        "vdot");
+    phase.set("drsdp:outer/eigen_step");
     // X = T - Diag(z) and its extreme eigenpairs: block Lanczos on
     // T V - z o V (partial decomposition) or the dense dsyevd; eta_max <= tol reported by
     // Lanczos is confirmed by one dense decomposition (the certificate never rests on Ritz values)
@@ -877,6 +885,7 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       ctx->trace.insert(ctx->trace.end(), row, row + 13);
       break;
     }
+    phase.set("drsdp:outer/rank_update");
     // escape directions: eigenvectors (Ritz vectors) with lambda < -eig_neg_tol (1 + |lambda_max|)
     const double thresh = -prm.eig_neg_tol * (1.0 + std::fabs(lam_top));
     int dv = 0;
@@ -1006,6 +1015,8 @@ static int solve_impl(drsdp_ctx *ctx, drsdp_info *info) {
       sig = std::max(run.sigma / prm.gamma, prm.sigma_min);
     else if (ratio > prm.tau2 * grad_paper)
       sig = std::min(prm.gamma * run.sigma, prm.sigma_max);
+    // reading R41: the dual residue is far ahead of the primal one -> raise the penalty
+    if (prm.sigma_boost > 0.0 && eta_d <= prm.sigma_boost * eta_p) sig = std::min(prm.gamma * run.sigma, prm.sigma_max);
     row[11] = dv;
     row[12] = now_s() - t0;
     ctx->trace.insert(ctx->trace.end(), row, row + 13);
