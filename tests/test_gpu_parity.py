@@ -538,6 +538,22 @@ def test_solve_preconditioned_against_oracle(ctx, d, seed):
     assert res["eta_max"] <= 1e-8
 
 
+def test_solve_sigma_boost_against_oracle(ctx):
+    """Reading R41 (penalty boost once eta_d <= sigma_boost * eta_p): the boosted solve reaches the same
+    certified optimum as the oracle's boosted solve, and the boost fires (sigma differs from the plain
+    Eq. 5.1 trajectory at some iteration)."""
+    Q, c = bqp_instance(10, 2)
+    info, sol, tr = _gpu_solve(ctx, Q, c, 2, 2, sigma_boost=0.5)
+    assert info["status"] == 0, info
+    amap, cnt, b = bqp.relax(Q, c)
+    o = admm.solve(amap, cnt, b, None, admm.Params(p0=2, sigma_boost=0.5), initial_factor(amap.shape[0], 2, 2))
+    assert o["status"] == "converged"
+    assert abs(info["dual_obj"] - o["dual_obj"]) <= 1e-6 * (1 + abs(o["dual_obj"]))
+    X = ctx.solution(want_X=True)["X"]
+    res = admm.residues(amap, cnt, b, None, sol["y"], sol["Y"], X + np.diag(sol["z"]))
+    assert res["eta_max"] <= 1e-8
+
+
 def test_solve_toy_q2(ctx):
     info, sol, tr = _gpu_solve(ctx, np.array([[0.0, 1.0], [1.0, 0.0]]), np.zeros(2), 2, 0)
     assert info["status"] == 0 and abs(info["dual_obj"] + 2.0) <= 1e-6

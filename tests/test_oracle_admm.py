@@ -180,3 +180,19 @@ def test_preconditioned_tcg_operator_and_solve():
         assert out["status"] == "converged" and out["eta_max"] <= 1e-8
         assert abs(out["dual_obj"] - ref["dual_obj"]) <= 1e-6 * (1 + abs(ref["dual_obj"]))
         assert out["dual_obj"] <= bqp.brute_force(Q, c)[0] + 1e-6
+
+
+def test_sigma_boost_reading_r41():
+    """Reading R41: with sigma_boost > 0 the penalty is raised whenever eta_d <= sigma_boost * eta_p
+    (whatever Eq. 5.1 says); the solve still reaches the brute-force-certified optimum of the tight d = 10
+    instance, and the sigma trajectory differs from the plain Eq. 5.1 one."""
+    Q, c, amap, cnt, b, prm, Y0 = _solve(10, 2, p0=2)
+    plain = admm.solve(amap, cnt, b, None, prm, Y0)
+    prm_b = admm.Params(p0=2, sigma_boost=0.5)
+    boosted = admm.solve(amap, cnt, b, None, prm_b, Y0)
+    assert boosted["status"] == "converged" and boosted["eta_max"] <= 1e-8
+    assert abs(boosted["dual_obj"] - plain["dual_obj"]) <= 1e-6 * (1 + abs(plain["dual_obj"]))
+    for r0, r1 in zip(boosted["trace"], boosted["trace"][1:]):
+        if r0["eta_d"] <= 0.5 * r0["eta_p"]:
+            assert r1["sigma"] == min(prm_b.gamma * r0["sigma"], prm_b.sigma_max)
+    assert [r["sigma"] for r in boosted["trace"]] != [r["sigma"] for r in plain["trace"]][:len(boosted["trace"])]

@@ -12,5 +12,10 @@ for fg in 0 1; do
   done
 done > gpurun_out/r2K_gather_solves.log 2>&1
 cat gpurun_out/r2K_gather_solves.log
+for sb in 1e-3 1e-2; do
+  echo "== sigma_boost=$sb d=40,60,80"
+  timeout 400 python tools/solve_run.py 40,60,80 150 4 sigma_boost=$sb 2>/dev/null | grep '^{' | cut -c1-330
+done > gpurun_out/r2K_boost_solves.log 2>&1
+cat gpurun_out/r2K_boost_solves.log
 timeout 600 ncu --nvtx --nvtx-include "drsdp:tcg/" --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
   --log-file gpurun_out/r2K_nvtx_tcg_launches.csv python tools/solve_run.py 40 60 4 > gpurun_out/r2K_nvtx.log 2>&1; tail -1 gpurun_out/r2K_nvtx.log | cut -c1-200
