@@ -88,10 +88,14 @@ int run_product(drsdp_ctx *ctx, SymvArgs &a, int epi, int mode2, bool atr, int p
     return set_error(ctx, DRSDP_ERR_INVALID_ARG,
                      "row-block product needs the TMA kernel (even pitch, 16 B aligned rows, p <= 64)");
   // matrix-light gather-product (f1): A*(w) gathered inside the ring from the TMA-loaded index-map panel;
-  // fused HVP epilogue for p <= 64 (DRSDP_FUSED_GATHER=0: off, =2: also the raw column chunks of p > 64)
+  // fused HVP epilogue for p <= 64. OFF by default (DRSDP_FUSED_GATHER=1: on, =2: also the raw column
+  // chunks of p > 64): the bitwise-repeatability stress test (tests/test_gpu_parity.py
+  // test_alm_hvp_bitwise_repeatable) found rare wrong tiles with the 8-gather-warp configuration at
+  // p <= 16 (a race not yet located; compute-sanitizer is refused by the pool), which also made the
+  // d = 70 / 80 solves nondeterministic and ~2x slower. The dense A*(w) path is bitwise repeatable.
   static const int fused_gather = [] {
     const char *e = std::getenv("DRSDP_FUSED_GATHER");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   if (!no_tma && fused_gather && mode2 == MODE2_GATHER && a.n >= 2048 && (epi == EPI_HVP || fused_gather >= 2) &&
       symv_gather_supported(a, epi, atr)) {

@@ -419,7 +419,7 @@ def _state_vectorised_map(d, kind, seed, sigma, p):
                                  (100, 512), (100, 1024), (70, 1536), (70, 2048), (150, 64)])
 def test_alm_eval_full_size(ctx, d, p):
     """BASELINE configs[1]/[2]/[3] sizes (n = 821, 5051, 11326): the y-eliminated evaluation in the
-    solver's launch configuration (dense Gram tiles + TMA products; for n >= 2048 and p <= 64 the
+    solver's launch configuration (dense Gram tiles + TMA products; for n >= 2048 and p <= 64, with DRSDP_FUSED_GATHER=1, the
     matrix-light HVP product of symv_gather.cu — every tile width 8 / 16 / 32 / 64, ragged n and p;
     p > 64 column-chunked products and row epilogues up to DRSDP_MAX_P) against the oracle."""
     from paper_2512_04406_b200 import abi
@@ -450,6 +450,36 @@ def test_alm_eval_full_size(ctx, d, p):
     assert rel(R.cpu().numpy(), o["R"], sE) <= TOL
     sH = sE + np.linalg.norm(4 * ops.At(amap, ops.A(amap, Y @ U.T + U @ Y.T, cnt.size) / cnt) @ Y)
     assert rel(H.cpu().numpy(), o["H"], sH) <= TOL
+
+
+@pytest.mark.parametrize("p", [8, 16, 32, 64])
+def test_alm_hvp_bitwise_repeatable(ctx, p):
+    """Race check for the matrix-light HVP product (symv_gather.cu: TMA ring shared by the producer,
+    the gather warps and the DMMA consumers, ticketed split-K): the kernel's summation order is
+    fixed, so 60 repetitions of the same ALM HVP at d = 80 (n = 3241) must agree bit for bit; a
+    missed barrier shows up as a run that differs. (compute-sanitizer is refused by the pool.)"""
+    from paper_2512_04406_b200 import abi
+
+    Q, c, amap, cnt, b, T, Y, U = _state_vectorised_map(80, "dense", 11, 2.0, p)
+    n = amap.shape[0]
+    ctx.set_bqp(Q, c)
+    ld = n + (-n) % 64
+    Tpad = np.zeros((n, ld))
+    Tpad[:, :n] = T
+    Td, Yd, Ud = dev(Tpad), dev(Y), dev(U)
+    cost = torch.zeros(1, dtype=torch.float64, device="cuda")
+    E, R = torch.empty_like(Yd), torch.empty_like(Yd)
+    ctx.alm_eval(abi.EVAL_COSTGRAD, p, Td, ld, 2.0, Yd, None, cost, E, R, None)
+    ref = None
+    for rep in range(60):
+        H = torch.full_like(Yd, float("nan"))
+        ctx.alm_eval(abi.EVAL_HVP, p, Td, ld, 2.0, Yd, Ud, None, None, None, H)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = H.clone()
+            assert torch.isfinite(ref).all()
+        else:
+            assert torch.equal(H, ref), f"repetition {rep} differs (max |diff| {(H - ref).abs().max().item():.3e})"
 
 
 @pytest.mark.parametrize("d,p", [(6, 3), (12, 7), (14, 70)])
